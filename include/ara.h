@@ -1,0 +1,215 @@
+/*
+ * ara.h -- C ABI of the B200-native aggregate risk analysis library (libara.so).
+ *
+ * The calls follow the paper's statement of the problem (arXiv 1308.2572, Sec. II):
+ *   inputs  : a Year Event Table (YET) of trials, Event Loss Tables (ELTs)
+ *             with per-ELT financial terms I (L49-L53), Layers = a set of ELTs plus layer terms
+ *             T = (OccR, OccL, AggR, AggL) (L55-L59);
+ *   method  : Algorithm 1 (L63-L112) -- per layer, per trial, per event: look up the event's
+ *             loss in every ELT of the layer (lines 4-7), apply financial terms (lines 8-10),
+ *             sum over ELTs (lines 11-13), apply occurrence terms (lines 15-17), take the running
+ *             sum over the trial's events (lines 18-20), apply aggregate terms (lines 21-23),
+ *             difference (lines 24-26) and sum (lines 27-29) into the trial loss lr;
+ *   outputs : the Year Loss Table (YLT) and, from a YLT, PML and TVaR (L32).
+ *
+ * Exact semantics (DESIGN.md "Readings" R1-R12; SPEC.md engine/metrics):
+ *   F_j(x)  = min(max(x * rate_j - retention_j, 0), limit_j)      (R1; * and - rounded apart)
+ *   lo_d    = ((0 + F_0(x_d0)) + F_1(x_d1)) + ... in the layer's ELT order (R7)
+ *   oc_d    = min(max(lo_d - OccR, 0), OccL)
+ *   S_d     = S_{d-1} + oc_d, S_0 = +0, in trial order (R5, R7)
+ *   C_d     = min(max(S_d - AggR, 0), AggL), C_0 = 0
+ *   lr      = (((0 + (C_1 - C_0)) + (C_2 - C_1)) + ...)            (R4, R5)
+ *   min(x,y) = (y < x ? y : x), max(x,0) = (x < 0 ? 0 : x); fp64, round-to-nearest-even, no FMA.
+ * The library reproduces these operations in this order, so its YLT is bit-identical to a
+ * sequential fp64 evaluation of Algorithm 1 (up to the sign of zero).
+ *
+ * Conventions
+ *   - Every call returns ara_status; no C++ exception crosses the ABI.  On failure nothing is
+ *     written to caller outputs and ara_last_error(ctx) names the offending item.
+ *   - Host arrays (h_ / unprefixed pointers in load/set calls) are caller-owned and read only
+ *     during the call.  Device arrays (d_) are caller-owned device memory of the context's
+ *     device; the library never frees or retains them beyond the call (or, for asynchronous
+ *     calls, beyond the stream-ordered completion of the enqueued work).
+ *   - The context owns every buffer it allocates (the device ELT store, staging buffers).
+ *   - Order: ara_create -> ara_load_elts -> ara_set_layers -> ara_run / ara_metrics.
+ *     ara_load_elts invalidates the layers (ARA_ERR_STATE until ara_set_layers is called).
+ *   - A context is not thread-safe; callers serialise calls on one context.
+ *     Distinct contexts may be used from distinct threads.
+ *   - Absent limits are +INFINITY.  Retentions and limits may not be NaN or negative.
+ */
+#ifndef ARA_H
+#define ARA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ara_ctx ara_ctx; /* opaque */
+
+typedef enum {
+    ARA_OK = 0,
+    ARA_ERR_ARG = 1,        /* NULL pointer, zero size where one is required, unknown flag   */
+    ARA_ERR_RANGE = 2,      /* event id 0 or > catalogue_size            */
+    ARA_ERR_VALIDATION = 3, /* bad terms, duplicate ids, non-monotone offsets, empty layer   */
+    ARA_ERR_STATE = 4,      /* call out of order (e.g. ara_run before ara_set_layers)        */
+    ARA_ERR_EMPTY = 5,      /* metrics over zero trials                       */
+    ARA_ERR_OOM = 6,        /* host or device allocation failed                              */
+    ARA_ERR_CUDA = 7,       /* CUDA runtime error (message in ara_last_error)                */
+    ARA_ERR_UNSUPPORTED = 8 /* a limit of this build (e.g. more than ARA_MAX_ELTS_PER_LAYER) */
+} ara_status;
+
+/* Financial terms I of one ELT (reading R1):
+ * rate > 0 finite (currency exchange rate), retention >= 0 finite, limit >= 0 or +INFINITY. */
+typedef struct {
+    double rate, retention, limit;
+} ara_fin_terms;
+
+/* Layer terms T: retentions >= 0 finite, limits >= 0 or +INF. */
+typedef struct {
+    double occ_retention, occ_limit, agg_retention, agg_limit;
+} ara_layer_terms;
+
+/* Limits of this build. */
+#define ARA_MAX_ELTS_PER_LAYER 64 /* "approximately 3 to 30" ELTs per layer  */
+#define ARA_MAX_P 32              /* probabilities per ara_metrics call                     */
+
+/* ara_run flags */
+#define ARA_RUN_SYNC 1u     /* wait for completion and report device-side errors           */
+#define ARA_RUN_VALIDATE 2u /* check offsets and event ids on the device BEFORE the scan
+                               (one extra YET read); implies ARA_RUN_SYNC; on error nothing
+                               is written to the YLT                                        */
+
+/* Human-readable name of a status code (static storage). */
+const char *ara_status_string(ara_status s);
+
+/* Create a context on CUDA device `cuda_device`.  `cuda_stream` is a cudaStream_t (or NULL for
+ * the legacy default stream) on which every asynchronous operation of the context is ordered;
+ * the caller keeps ownership of the stream.  *out receives the context. */
+ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out);
+
+/* Change the stream of an existing context (caller-owned cudaStream_t or NULL). */
+ara_status ara_set_stream(ara_ctx *ctx, void *cuda_stream);
+
+/* Release the context and every buffer it owns.  NULL is a no-op. */
+void ara_destroy(ara_ctx *ctx);
+
+/* Message describing the last failed call on ctx ("" if none).  Valid until the next call. */
+const char *ara_last_error(const ara_ctx *ctx);
+
+/*
+ * ara_load_elts -- the second input of PAPER.md Sec. II: ELTs as CSR over records.
+ *   catalogue_size        number of events in the global catalogue C (ids are 1..C)
+ *   n_elts                number of ELTs (>= 1)
+ *   rec_offsets[n_elts+1] non-decreasing; ELT j's records are [rec_offsets[j], rec_offsets[j+1])
+ *   rec_event_ids[]       event id of each record, in [1, C], unique within an ELT
+ *   rec_losses[]          loss l_i of each record, finite and >= 0 (0 is the same as absent)
+ *   fin[n_elts]           financial terms of each ELT
+ * Copies what it needs; the arrays may be freed afterwards.  Invalidates any layers.
+ * Errors: ARA_ERR_ARG, ARA_ERR_RANGE (id 0 or > C), ARA_ERR_VALIDATION (duplicate id in an
+ * ELT, bad loss or terms, decreasing offsets), ARA_ERR_OOM.
+ */
+ara_status ara_load_elts(ara_ctx *ctx, uint32_t catalogue_size, uint32_t n_elts,
+                         const uint64_t *rec_offsets, const uint32_t *rec_event_ids,
+                         const double *rec_losses, const ara_fin_terms *fin);
+
+/*
+ * ara_set_layers -- the third input of PAPER.md Sec. II (L55-L59) and the preprocessing stage
+ * of Algorithm 1 (L61): builds, per layer, the device ELT store:
+ *   map[0..C]  (u32)  catalogue id -> dense row, 0 = event in none of the layer's ELTs
+ *   rows[0..U][W]     fp64, row r = the losses of the r-th event of the union U of the layer's
+ *                     ELT events, column j = the layer's j-th ELT (0 where absent); row 0 zero;
+ *                     W = |E_l| rounded up to whole 32-byte chunks: 4, 8 or a multiple of
+ *                     16 doubles (row_width_for in csrc/ara_internal.h)
+ * i.e. the paper's direct access tables (L124) re-laid-out event-major and compacted.
+ *   n_layers               >= 1
+ *   terms[n_layers]        layer terms T
+ *   elt_offsets[n_layers+1] non-decreasing; layer l covers elt_index[elt_offsets[l] ..
+ *                          elt_offsets[l+1]), non-empty, at most ARA_MAX_ELTS_PER_LAYER
+ *   elt_index[]            ELT numbers < n_elts, distinct within a layer; the listed order is
+ *                          the summation order of Alg. 1 lines 11-13
+ * Errors: ARA_ERR_STATE (no ELTs), ARA_ERR_ARG, ARA_ERR_VALIDATION, ARA_ERR_UNSUPPORTED,
+ * ARA_ERR_OOM, ARA_ERR_CUDA.  Synchronous.
+ */
+ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms *terms,
+                          const uint32_t *elt_offsets, const uint32_t *elt_index);
+
+/*
+ * ara_run -- Algorithm 1 lines 2-29 over a device-resident YET: YET -> YLT.
+ *   n_trials                  number of trials (0 is a no-op)
+ *   d_trial_offsets[n+1]      device, u64, non-decreasing; trial t's events are
+ *                             d_event_ids[d_trial_offsets[t] - d_trial_offsets[0] ...
+ *                             d_trial_offsets[t+1] - d_trial_offsets[0]) in ascending time order
+ *                             (only the order is used: PAPER.md L42; timestamps are not taken)
+ *   d_event_ids[]             device, u32 catalogue ids in [1, C]
+ *   d_ylt                     device, fp64, YLT[l][t] at d_ylt[l * ylt_ld + t]
+ *   ylt_ld                    row stride of the YLT in elements (0 means n_trials)
+ *   flags                     ARA_RUN_SYNC | ARA_RUN_VALIDATE
+ * Without ARA_RUN_SYNC the call only enqueues work on the context stream and returns ARA_OK;
+ * an event id outside [1, C] then reads the zero row (never out of bounds) and sets a device
+ * error flag that the next ara_synchronize() (or synchronous call) reports as ARA_ERR_RANGE.
+ * Errors: ARA_ERR_STATE, ARA_ERR_ARG, ARA_ERR_RANGE, ARA_ERR_VALIDATION, ARA_ERR_CUDA.
+ */
+ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
+                   const uint32_t *d_event_ids, double *d_ylt, uint64_t ylt_ld, uint32_t flags);
+
+/*
+ * ara_run_host -- ara_run with HOST buffers (end-to-end path): h_trial_offsets[n+1] and
+ * h_event_ids as in ara_run but in host memory (page-locked memory gives full PCIe bandwidth),
+ * h_ylt[l * ylt_ld + t] in host memory.  The YET is streamed to the device in chunks on the
+ * context stream and a copy stream, overlapping copies with the scan.  Synchronous.
+ * Errors: as ara_run (validation of ids is always performed on the device).
+ */
+ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial_offsets,
+                        const uint32_t *h_event_ids, double *h_ylt, uint64_t ylt_ld,
+                        uint32_t flags);
+
+/* Wait for all work enqueued on the context stream; report deferred device errors. */
+ara_status ara_synchronize(ara_ctx *ctx);
+
+/*
+ * ara_metrics -- PML and TVaR of one YLT row (reading R11):
+ *   PML(p)  = v[ceil(p * n) - 1] of the row sorted ascending (nearest rank)
+ *   TVaR(p) = mean of all v >= PML(p)
+ *   d_ylt_row[n]   device, fp64, finite
+ *   p[n_p]         host, each in (0, 1), n_p <= ARA_MAX_P
+ *   pml_out, tvar_out  host, [n_p]
+ * Computed on the device (radix select + tail mean); synchronous.
+ * Errors: ARA_ERR_EMPTY (n == 0), ARA_ERR_ARG (p outside (0,1), n_p == 0 or > ARA_MAX_P),
+ * ARA_ERR_CUDA.
+ */
+ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32_t n_p,
+                       const double *p, double *pml_out, double *tvar_out);
+
+/* ara_metrics on a HOST YLT row (copied to the device first).  Synchronous. */
+ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, uint32_t n_p,
+                            const double *p, double *pml_out, double *tvar_out);
+
+/* Introspection (tests, benchmarks). */
+typedef struct {
+    uint32_t catalogue_size;
+    uint32_t n_elts;
+    uint32_t n_layers;
+    uint32_t max_row_width;      /* max W over layers (doubles per row)                  */
+    uint64_t store_bytes;        /* device bytes of maps + rows of all layers            */
+    uint64_t kernel_launches;    /* kernels launched by this context so far               */
+    int device;
+    int sm_count;
+} ara_info;
+
+ara_status ara_get_info(const ara_ctx *ctx, ara_info *out);
+
+/* Per-layer store shape: number of union events U (rows = U + 1) and row width W. */
+ara_status ara_layer_store_shape(const ara_ctx *ctx, uint32_t layer, uint32_t *n_union,
+                                 uint32_t *row_width);
+
+/* Copy a layer's device store back to the host (store round-trip tests):
+ * h_map[C+1] (u32) and h_rows[(U+1) * W] (fp64).  Either pointer may be NULL.  Synchronous. */
+ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, double *h_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARA_H */

@@ -1,0 +1,616 @@
+// ara.cpp -- host side of libara: the C ABI of include/ara.h.
+//
+// Context state machine, input validation (SPEC.md core-model rules), the device ELT store
+// build of ara_set_layers (A1: event-major rows + catalogue map),
+// and orchestration of the scan (A2-A8) and metrics (A9) kernels on the context stream.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ara.h"
+#include "ara_internal.h"
+
+struct ara_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::string err;
+
+    bool have_elts = false;
+    bool have_layers = false;
+    uint32_t C = 0;
+    uint32_t n_elts = 0;
+    std::vector<uint64_t> rec_off;
+    std::vector<uint32_t> rec_ids;
+    std::vector<double> rec_losses;
+    std::vector<ara_fin_terms> fin;
+
+    std::vector<ara::DeviceLayer> layers;
+    uint64_t store_bytes = 0;
+
+    uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
+    uint32_t *h_err = nullptr;  // pinned mirror
+    uint64_t launches = 0;
+    ara::MetricsScratch metrics;
+
+    // ara_run_host staging (double-buffered)
+    uint32_t *d_ids_stage[2] = {nullptr, nullptr};
+    uint64_t *d_off_stage[2] = {nullptr, nullptr};
+    size_t ids_stage_cap = 0;   // u32 elements per buffer
+    size_t off_stage_cap = 0;   // u64 elements per buffer
+    double *d_ylt_stage = nullptr;
+    size_t ylt_stage_cap = 0;
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
+    double *d_row_stage = nullptr;  // ara_metrics_host
+    size_t row_stage_cap = 0;
+};
+
+namespace {
+
+ara_status fail(ara_ctx *ctx, ara_status s, const char *fmt, ...)
+{
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return s;
+}
+
+ara_status cuda_fail(ara_ctx *ctx, cudaError_t e, const char *what)
+{
+    return fail(ctx, e == cudaErrorMemoryAllocation ? ARA_ERR_OOM : ARA_ERR_CUDA, "%s: %s (%s)",
+                what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define ARA_CUDA(ctx, call)                                   \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool finite_nonneg(double x) { return isfinite(x) && x >= 0.0; }
+bool limit_ok(double x) { return !isnan(x) && x >= 0.0; }  // +inf allowed
+
+void free_layers(ara_ctx *ctx)
+{
+    for (auto &L : ctx->layers) {
+        cudaFree(L.d_map);
+        cudaFree(L.d_rows);
+    }
+    ctx->layers.clear();
+    ctx->store_bytes = 0;
+    ctx->have_layers = false;
+}
+
+template <typename F>
+ara_status guarded(ara_ctx *ctx, F &&f)
+{
+    if (!ctx) return ARA_ERR_ARG;
+    try {
+        ctx->err.clear();
+        DeviceGuard g(ctx->device);
+        return f();
+    } catch (const std::bad_alloc &) {
+        return fail(ctx, ARA_ERR_OOM, "host allocation failed");
+    } catch (...) {
+        return fail(ctx, ARA_ERR_ARG, "unexpected exception");
+    }
+}
+
+ara_status validate_p(ara_ctx *ctx, uint32_t n_p, const double *p)
+{
+    if (n_p == 0 || n_p > ARA_MAX_P)
+        return fail(ctx, ARA_ERR_ARG, "n_p = %u outside [1, %d]", n_p, ARA_MAX_P);
+    if (!p) return fail(ctx, ARA_ERR_ARG, "p is NULL");
+    for (uint32_t i = 0; i < n_p; ++i)
+        if (!(p[i] > 0.0 && p[i] < 1.0))
+            return fail(ctx, ARA_ERR_ARG, "p[%u] = %g outside (0, 1)", i, p[i]);
+    return ARA_OK;
+}
+
+ara_status check_device_error(ara_ctx *ctx)
+{
+    ARA_CUDA(ctx, cudaMemcpyAsync(ctx->h_err, ctx->d_err, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const uint32_t e = *ctx->h_err;
+    if (e) {
+        ARA_CUDA(ctx, cudaMemsetAsync(ctx->d_err, 0, 4, ctx->stream));
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (e & ara::kErrOffsets)
+            return fail(ctx, ARA_ERR_VALIDATION, "trial offsets are decreasing");
+        return fail(ctx, ARA_ERR_RANGE, "a trial event id is 0 or exceeds the catalogue (%u)",
+                    ctx->C);
+    }
+    return ARA_OK;
+}
+
+ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const uint32_t *d_ids,
+                         double *d_ylt, uint64_t ld)
+{
+    for (size_t l = 0; l < ctx->layers.size(); ++l) {
+        ara::ScanLaunch s{d_off, d_ids, d_ylt + l * ld, n, ctx->C, ctx->d_err};
+        cudaError_t e = ara::launch_scan(ctx->layers[l], s, ctx->sm_count, ctx->stream,
+                                         &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
+    }
+    return ARA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ara_status_string(ara_status s)
+{
+    switch (s) {
+        case ARA_OK: return "ARA_OK";
+        case ARA_ERR_ARG: return "ARA_ERR_ARG";
+        case ARA_ERR_RANGE: return "ARA_ERR_RANGE";
+        case ARA_ERR_VALIDATION: return "ARA_ERR_VALIDATION";
+        case ARA_ERR_STATE: return "ARA_ERR_STATE";
+        case ARA_ERR_EMPTY: return "ARA_ERR_EMPTY";
+        case ARA_ERR_OOM: return "ARA_ERR_OOM";
+        case ARA_ERR_CUDA: return "ARA_ERR_CUDA";
+        case ARA_ERR_UNSUPPORTED: return "ARA_ERR_UNSUPPORTED";
+    }
+    return "ARA_ERR_UNKNOWN";
+}
+
+ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
+{
+    if (!out) return ARA_ERR_ARG;
+    *out = nullptr;
+    int n_dev = 0;
+    if (cudaGetDeviceCount(&n_dev) != cudaSuccess || cuda_device < 0 || cuda_device >= n_dev)
+        return ARA_ERR_CUDA;
+    ara_ctx *ctx = new (std::nothrow) ara_ctx();
+    if (!ctx) return ARA_ERR_OOM;
+    ctx->device = cuda_device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    DeviceGuard g(cuda_device);
+    cudaError_t e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount,
+                                           cuda_device);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 4);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, 4);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+        e = cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_done[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        ara_destroy(ctx);
+        return e == cudaErrorMemoryAllocation ? ARA_ERR_OOM : ARA_ERR_CUDA;
+    }
+    *out = ctx;
+    return ARA_OK;
+}
+
+ara_status ara_set_stream(ara_ctx *ctx, void *cuda_stream)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        ctx->stream = (cudaStream_t)cuda_stream;
+        return ARA_OK;
+    });
+}
+
+void ara_destroy(ara_ctx *ctx)
+{
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    free_layers(ctx);
+    cudaFree(ctx->d_err);
+    cudaFreeHost(ctx->h_err);
+    cudaFree(ctx->metrics.d_buf);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(ctx->d_ids_stage[i]);
+        cudaFree(ctx->d_off_stage[i]);
+        if (ctx->ev_copy[i]) cudaEventDestroy(ctx->ev_copy[i]);
+        if (ctx->ev_done[i]) cudaEventDestroy(ctx->ev_done[i]);
+    }
+    cudaFree(ctx->d_ylt_stage);
+    cudaFree(ctx->d_row_stage);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+}
+
+const char *ara_last_error(const ara_ctx *ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+ara_status ara_load_elts(ara_ctx *ctx, uint32_t catalogue_size, uint32_t n_elts,
+                         const uint64_t *rec_offsets, const uint32_t *rec_event_ids,
+                         const double *rec_losses, const ara_fin_terms *fin)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (catalogue_size == 0 || catalogue_size == UINT32_MAX)
+            return fail(ctx, ARA_ERR_ARG, "catalogue_size %u outside [1, 2^32-2]", catalogue_size);
+        if (n_elts == 0) return fail(ctx, ARA_ERR_ARG, "n_elts is 0");
+        if (!rec_offsets || !fin) return fail(ctx, ARA_ERR_ARG, "rec_offsets or fin is NULL");
+        for (uint32_t j = 0; j < n_elts; ++j)
+            if (rec_offsets[j + 1] < rec_offsets[j])
+                return fail(ctx, ARA_ERR_VALIDATION, "rec_offsets decrease at ELT %u", j);
+        const uint64_t base = rec_offsets[0];
+        const uint64_t n_rec = rec_offsets[n_elts] - base;
+        if (n_rec && (!rec_event_ids || !rec_losses))
+            return fail(ctx, ARA_ERR_ARG, "record arrays are NULL");
+        for (uint32_t j = 0; j < n_elts; ++j) {
+            const ara_fin_terms &f = fin[j];
+            if (!(isfinite(f.rate) && f.rate > 0.0))
+                return fail(ctx, ARA_ERR_VALIDATION, "ELT %u: rate %g is not finite and > 0", j,
+                            f.rate);
+            if (!finite_nonneg(f.retention))
+                return fail(ctx, ARA_ERR_VALIDATION, "ELT %u: retention %g is not finite and >= 0",
+                            j, f.retention);
+            if (!limit_ok(f.limit))
+                return fail(ctx, ARA_ERR_VALIDATION, "ELT %u: limit %g is not >= 0 (or +inf)", j,
+                            f.limit);
+        }
+        std::vector<uint32_t> stamp((size_t)catalogue_size + 1, 0);
+        for (uint32_t j = 0; j < n_elts; ++j) {
+            for (uint64_t r = rec_offsets[j] - base; r < rec_offsets[j + 1] - base; ++r) {
+                const uint32_t id = rec_event_ids[r];
+                if (id == 0 || id > catalogue_size)
+                    return fail(ctx, ARA_ERR_RANGE,
+                                "ELT %u record %llu: event id %u outside [1, %u]", j,
+                                (unsigned long long)(r - (rec_offsets[j] - base)), id,
+                                catalogue_size);
+                if (stamp[id] == j + 1)
+                    return fail(ctx, ARA_ERR_VALIDATION, "ELT %u: duplicate event id %u", j, id);
+                stamp[id] = j + 1;
+                if (!finite_nonneg(rec_losses[r]))
+                    return fail(ctx, ARA_ERR_VALIDATION,
+                                "ELT %u record %llu: loss %g is not finite and >= 0", j,
+                                (unsigned long long)(r - (rec_offsets[j] - base)), rec_losses[r]);
+            }
+        }
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        free_layers(ctx);
+        ctx->C = catalogue_size;
+        ctx->n_elts = n_elts;
+        ctx->rec_off.assign(rec_offsets, rec_offsets + n_elts + 1);
+        for (auto &o : ctx->rec_off) o -= base;
+        ctx->rec_ids.assign(rec_event_ids, rec_event_ids + n_rec);
+        ctx->rec_losses.assign(rec_losses, rec_losses + n_rec);
+        ctx->fin.assign(fin, fin + n_elts);
+        ctx->have_elts = true;
+        return ARA_OK;
+    });
+}
+
+ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms *terms,
+                          const uint32_t *elt_offsets, const uint32_t *elt_index)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (!ctx->have_elts) return fail(ctx, ARA_ERR_STATE, "ara_load_elts has not succeeded");
+        if (n_layers == 0) return fail(ctx, ARA_ERR_ARG, "n_layers is 0");
+        if (!terms || !elt_offsets || !elt_index)
+            return fail(ctx, ARA_ERR_ARG, "terms, elt_offsets or elt_index is NULL");
+        std::vector<uint32_t> stamp(ctx->n_elts, 0);
+        for (uint32_t l = 0; l < n_layers; ++l) {
+            const ara_layer_terms &t = terms[l];
+            if (!finite_nonneg(t.occ_retention) || !finite_nonneg(t.agg_retention))
+                return fail(ctx, ARA_ERR_VALIDATION, "layer %u: retentions must be finite and >= 0",
+                            l);
+            if (!limit_ok(t.occ_limit) || !limit_ok(t.agg_limit))
+                return fail(ctx, ARA_ERR_VALIDATION, "layer %u: limits must be >= 0 (or +inf)", l);
+            if (elt_offsets[l + 1] < elt_offsets[l])
+                return fail(ctx, ARA_ERR_VALIDATION, "elt_offsets decrease at layer %u", l);
+            const uint32_t E = elt_offsets[l + 1] - elt_offsets[l];
+            if (E == 0) return fail(ctx, ARA_ERR_VALIDATION, "layer %u covers no ELT", l);
+            if (E > ARA_MAX_ELTS_PER_LAYER)
+                return fail(ctx, ARA_ERR_UNSUPPORTED, "layer %u covers %u ELTs (max %d)", l, E,
+                            ARA_MAX_ELTS_PER_LAYER);
+            for (uint32_t c = elt_offsets[l]; c < elt_offsets[l + 1]; ++c) {
+                const uint32_t j = elt_index[c];
+                if (j >= ctx->n_elts)
+                    return fail(ctx, ARA_ERR_VALIDATION, "layer %u: ELT index %u >= n_elts %u", l,
+                                j, ctx->n_elts);
+                if (stamp[j] == l + 1)
+                    return fail(ctx, ARA_ERR_VALIDATION, "layer %u lists ELT %u twice", l, j);
+                stamp[j] = l + 1;
+            }
+        }
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        free_layers(ctx);
+
+        const uint32_t C = ctx->C;
+        std::vector<uint32_t> map((size_t)C + 1);
+        std::vector<uint32_t> seen((size_t)C + 1, 0);
+        for (uint32_t l = 0; l < n_layers; ++l) {
+            ara::DeviceLayer L;
+            const uint32_t E = elt_offsets[l + 1] - elt_offsets[l];
+            const uint32_t W = ara::row_width_for(E);
+            L.n_cols = E;
+            L.width = W;
+            if (const char *g = getenv("ARA_SCAN_GROUP")) L.group_override = atoi(g);
+            // union of the layer's events, ascending id -> dense rows 1..U
+            std::vector<uint32_t> uni;
+            for (uint32_t c = 0; c < E; ++c) {
+                const uint32_t j = elt_index[elt_offsets[l] + c];
+                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r) {
+                    const uint32_t id = ctx->rec_ids[r];
+                    if (seen[id] != l + 1) {
+                        seen[id] = l + 1;
+                        uni.push_back(id);
+                    }
+                }
+            }
+            std::sort(uni.begin(), uni.end());
+            L.n_union = (uint32_t)uni.size();
+            std::fill(map.begin(), map.end(), 0u);
+            for (uint32_t u = 0; u < L.n_union; ++u) map[uni[u]] = u + 1;
+            std::vector<double> rows((size_t)(L.n_union + 1) * W, 0.0);
+            for (uint32_t c = 0; c < E; ++c) {
+                const uint32_t j = elt_index[elt_offsets[l] + c];
+                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
+                    rows[(size_t)map[ctx->rec_ids[r]] * W + c] = ctx->rec_losses[r];  // bit copy
+                L.terms.rate[c] = ctx->fin[j].rate;
+                L.terms.ret[c] = ctx->fin[j].retention;
+                L.terms.lim[c] = ctx->fin[j].limit;
+            }
+            for (uint32_t c = E; c < ara::kMaxCols; ++c) {  // neutral padding columns
+                L.terms.rate[c] = 1.0;
+                L.terms.ret[c] = 0.0;
+                L.terms.lim[c] = INFINITY;
+            }
+            L.terms.occ_ret = terms[l].occ_retention;
+            L.terms.occ_lim = terms[l].occ_limit;
+            L.terms.agg_ret = terms[l].agg_retention;
+            L.terms.agg_lim = terms[l].agg_limit;
+            const size_t map_bytes = ((size_t)C + 1) * 4, row_bytes = rows.size() * 8;
+            cudaError_t e = cudaMalloc(&L.d_map, map_bytes);
+            if (e == cudaSuccess) e = cudaMalloc(&L.d_rows, row_bytes);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(L.d_map, map.data(), map_bytes, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(L.d_rows, rows.data(), row_bytes, cudaMemcpyHostToDevice);
+            ctx->layers.push_back(L);
+            if (e != cudaSuccess) {
+                free_layers(ctx);
+                return cuda_fail(ctx, e, "device ELT store");
+            }
+            ctx->store_bytes += map_bytes + row_bytes;
+        }
+        ctx->have_layers = true;
+        return ARA_OK;
+    });
+}
+
+ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
+                   const uint32_t *d_event_ids, double *d_ylt, uint64_t ylt_ld, uint32_t flags)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE))
+            return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
+        if (n_trials == 0) return ARA_OK;
+        if (!d_trial_offsets || !d_event_ids || !d_ylt)
+            return fail(ctx, ARA_ERR_ARG, "device pointer is NULL");
+        const uint64_t ld = ylt_ld ? ylt_ld : n_trials;
+        if (ld < n_trials) return fail(ctx, ARA_ERR_ARG, "ylt_ld %llu < n_trials", (unsigned long long)ld);
+        if (flags & ARA_RUN_VALIDATE) {
+            ara_status s = check_device_error(ctx);  // report earlier deferred errors first
+            if (s != ARA_OK) return s;
+            cudaError_t e = ara::launch_validate(d_trial_offsets, d_event_ids, n_trials, ctx->C,
+                                                 ctx->d_err, ctx->sm_count, ctx->stream,
+                                                 &ctx->launches);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "validate kernel launch");
+            s = check_device_error(ctx);
+            if (s != ARA_OK) return s;
+        }
+        ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, d_ylt, ld);
+        if (s != ARA_OK) return s;
+        if (flags & (ARA_RUN_SYNC | ARA_RUN_VALIDATE)) return check_device_error(ctx);
+        return ARA_OK;
+    });
+}
+
+ara_status ara_synchronize(ara_ctx *ctx)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        ARA_CUDA(ctx, cudaGetLastError());
+        return check_device_error(ctx);
+    });
+}
+
+ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial_offsets,
+                        const uint32_t *h_event_ids, double *h_ylt, uint64_t ylt_ld,
+                        uint32_t flags)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE))
+            return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
+        if (n_trials == 0) return ARA_OK;
+        if (!h_trial_offsets || !h_ylt) return fail(ctx, ARA_ERR_ARG, "host pointer is NULL");
+        const uint64_t ld = ylt_ld ? ylt_ld : n_trials;
+        if (ld < n_trials) return fail(ctx, ARA_ERR_ARG, "ylt_ld < n_trials");
+        for (uint64_t t = 0; t < n_trials; ++t)
+            if (h_trial_offsets[t + 1] < h_trial_offsets[t])
+                return fail(ctx, ARA_ERR_VALIDATION, "trial offsets decrease at trial %llu",
+                            (unsigned long long)t);
+        const uint64_t base = h_trial_offsets[0];
+        if (h_trial_offsets[n_trials] > base && !h_event_ids)
+            return fail(ctx, ARA_ERR_ARG, "h_event_ids is NULL");
+        ara_status s = check_device_error(ctx);
+        if (s != ARA_OK) return s;
+
+        const size_t n_layers = ctx->layers.size();
+        // device YLT staging
+        if (ctx->ylt_stage_cap < n_layers * n_trials) {
+            cudaFree(ctx->d_ylt_stage);
+            ctx->d_ylt_stage = nullptr;
+            ctx->ylt_stage_cap = 0;
+            ARA_CUDA(ctx, cudaMalloc(&ctx->d_ylt_stage, n_layers * n_trials * 8));
+            ctx->ylt_stage_cap = n_layers * n_trials;
+        }
+        // chunking at trial boundaries: ~64 MiB of ids per chunk (>= 1 trial)
+        const size_t kChunkIds = (size_t)16 << 20;
+        uint64_t max_trial = 0;
+        for (uint64_t t = 0; t < n_trials; ++t)
+            max_trial = std::max<uint64_t>(max_trial, h_trial_offsets[t + 1] - h_trial_offsets[t]);
+        const size_t ids_cap = std::max<size_t>(kChunkIds, max_trial);
+        const size_t off_cap = ids_cap + 2;  // a chunk holds at most ids_cap non-empty trials...
+        if (ctx->ids_stage_cap < ids_cap || ctx->off_stage_cap < off_cap) {
+            for (int i = 0; i < 2; ++i) {
+                cudaFree(ctx->d_ids_stage[i]);
+                cudaFree(ctx->d_off_stage[i]);
+                ctx->d_ids_stage[i] = nullptr;
+                ctx->d_off_stage[i] = nullptr;
+            }
+            ctx->ids_stage_cap = ctx->off_stage_cap = 0;
+            for (int i = 0; i < 2; ++i) {
+                ARA_CUDA(ctx, cudaMalloc(&ctx->d_ids_stage[i], ids_cap * 4));
+                ARA_CUDA(ctx, cudaMalloc(&ctx->d_off_stage[i], off_cap * 8));
+            }
+            ctx->ids_stage_cap = ids_cap;
+            ctx->off_stage_cap = off_cap;
+        }
+        // ... and at most off_cap - 1 trials (empty trials)
+        uint64_t t0 = 0;
+        int buf = 0;
+        bool used[2] = {false, false};
+        while (t0 < n_trials) {
+            uint64_t t1 = t0 + 1;
+            while (t1 < n_trials && t1 - t0 < off_cap - 1 &&
+                   h_trial_offsets[t1 + 1] - h_trial_offsets[t0] <= ids_cap)
+                ++t1;
+            const uint64_t n_ev = h_trial_offsets[t1] - h_trial_offsets[t0];
+            if (used[buf]) ARA_CUDA(ctx, cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_done[buf], 0));
+            ARA_CUDA(ctx, cudaMemcpyAsync(ctx->d_off_stage[buf], h_trial_offsets + t0,
+                                          (t1 - t0 + 1) * 8, cudaMemcpyHostToDevice,
+                                          ctx->copy_stream));
+            if (n_ev)
+                ARA_CUDA(ctx, cudaMemcpyAsync(ctx->d_ids_stage[buf],
+                                              h_event_ids + (h_trial_offsets[t0] - base),
+                                              n_ev * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
+            ARA_CUDA(ctx, cudaEventRecord(ctx->ev_copy[buf], ctx->copy_stream));
+            ARA_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copy[buf], 0));
+            s = launch_layers(ctx, t1 - t0, ctx->d_off_stage[buf], ctx->d_ids_stage[buf],
+                              ctx->d_ylt_stage + t0, n_trials);
+            if (s != ARA_OK) return s;
+            ARA_CUDA(ctx, cudaEventRecord(ctx->ev_done[buf], ctx->stream));
+            used[buf] = true;
+            buf ^= 1;
+            t0 = t1;
+        }
+        ARA_CUDA(ctx, cudaMemcpy2DAsync(h_ylt, ld * 8, ctx->d_ylt_stage, n_trials * 8,
+                                        n_trials * 8, n_layers, cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+        return check_device_error(ctx);
+    });
+}
+
+ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32_t n_p,
+                       const double *p, double *pml_out, double *tvar_out)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
+        ara_status s = validate_p(ctx, n_p, p);
+        if (s != ARA_OK) return s;
+        if (!d_ylt_row || !pml_out || !tvar_out) return fail(ctx, ARA_ERR_ARG, "NULL pointer");
+        cudaError_t e = ara::launch_metrics(d_ylt_row, n, n_p, p, pml_out, tvar_out, ctx->metrics,
+                                            ctx->sm_count, ctx->device, ctx->stream,
+                                            &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");
+        return ARA_OK;
+    });
+}
+
+ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, uint32_t n_p,
+                            const double *p, double *pml_out, double *tvar_out)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
+        ara_status s = validate_p(ctx, n_p, p);
+        if (s != ARA_OK) return s;
+        if (!h_ylt_row || !pml_out || !tvar_out) return fail(ctx, ARA_ERR_ARG, "NULL pointer");
+        if (ctx->row_stage_cap < n) {
+            cudaFree(ctx->d_row_stage);
+            ctx->d_row_stage = nullptr;
+            ctx->row_stage_cap = 0;
+            ARA_CUDA(ctx, cudaMalloc(&ctx->d_row_stage, n * 8));
+            ctx->row_stage_cap = n;
+        }
+        ARA_CUDA(ctx, cudaMemcpyAsync(ctx->d_row_stage, h_ylt_row, n * 8, cudaMemcpyHostToDevice,
+                                      ctx->stream));
+        cudaError_t e = ara::launch_metrics(ctx->d_row_stage, n, n_p, p, pml_out, tvar_out,
+                                            ctx->metrics, ctx->sm_count, ctx->device,
+                                            ctx->stream, &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");
+        return ARA_OK;
+    });
+}
+
+ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
+{
+    if (!ctx || !out) return ARA_ERR_ARG;
+    out->catalogue_size = ctx->C;
+    out->n_elts = ctx->n_elts;
+    out->n_layers = ctx->have_layers ? (uint32_t)ctx->layers.size() : 0;
+    out->max_row_width = 0;
+    for (auto &L : ctx->layers) out->max_row_width = std::max(out->max_row_width, L.width);
+    out->store_bytes = ctx->store_bytes;
+    out->kernel_launches = ctx->launches;
+    out->device = ctx->device;
+    out->sm_count = ctx->sm_count;
+    return ARA_OK;
+}
+
+ara_status ara_layer_store_shape(const ara_ctx *ctx, uint32_t layer, uint32_t *n_union,
+                                 uint32_t *row_width)
+{
+    if (!ctx) return ARA_ERR_ARG;
+    if (!ctx->have_layers) return ARA_ERR_STATE;
+    if (layer >= ctx->layers.size()) return ARA_ERR_ARG;
+    if (n_union) *n_union = ctx->layers[layer].n_union;
+    if (row_width) *row_width = ctx->layers[layer].width;
+    return ARA_OK;
+}
+
+ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, double *h_rows)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "no layers");
+        if (layer >= ctx->layers.size()) return fail(ctx, ARA_ERR_ARG, "layer %u out of range", layer);
+        const ara::DeviceLayer &L = ctx->layers[layer];
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (h_map)
+            ARA_CUDA(ctx, cudaMemcpy(h_map, L.d_map, ((size_t)ctx->C + 1) * 4, cudaMemcpyDeviceToHost));
+        if (h_rows)
+            ARA_CUDA(ctx, cudaMemcpy(h_rows, L.d_rows, (size_t)(L.n_union + 1) * L.width * 8,
+                                     cudaMemcpyDeviceToHost));
+        return ARA_OK;
+    });
+}
+
+}  // extern "C"

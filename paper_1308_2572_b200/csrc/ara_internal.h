@@ -1,0 +1,93 @@
+// ara_internal.h -- shared declarations of libara's host code (ara.cpp) and kernels
+// (scan.cu, metrics.cu).  Not installed; the public ABI is include/ara.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "ara.h"
+
+namespace ara {
+
+constexpr int kMaxCols = ARA_MAX_ELTS_PER_LAYER;  // row width limit W (doubles)
+
+// Per-layer terms, passed by value as a kernel parameter (lives in the constant bank: every
+// lane reads the same address, the broadcast the paper got from constant memory, PAPER.md
+// L132).  Padded columns j >= E carry the neutral terms (rate 1, retention 0, limit +inf)
+// and zero losses, so F_j = +0 and lo + (+0) = lo exactly.
+struct ScanTerms {
+    double rate[kMaxCols];
+    double ret[kMaxCols];
+    double lim[kMaxCols];
+    double occ_ret, occ_lim, agg_ret, agg_lim;
+};
+
+// Scan decomposition for a row width: G lanes per trial, each owning CH 32-byte chunks
+// (4 doubles each), W = 4 * G * CH.  The paper's 15-16 ELT layers give W = 16, G = 4: one
+// 128-byte row per group, one 256-bit load per lane.
+struct ScanShape {
+    int G, CH;
+};
+
+// Row width (doubles) of the event-major store for a layer of E ELTs.
+inline uint32_t row_width_for(uint32_t E)
+{
+    const uint32_t nc = (E + 3) / 4;  // 32-byte chunks needed
+    if (nc <= 1) return 4;
+    if (nc == 2) return 8;
+    return 16 * ((nc + 3) / 4);       // G = 4, CH = ceil(nc / 4)
+}
+
+// Decomposition for a store of width W; override (1, 2 or 4) selects G for W = 16 only.
+inline ScanShape scan_shape_for_width(uint32_t W, int override_g)
+{
+    if (W == 4) return {1, 1};
+    if (W == 8) return {2, 1};
+    if (W == 16 && (override_g == 1 || override_g == 2)) return {override_g, 4 / override_g};
+    return {4, (int)(W / 16)};
+}
+
+// Device ELT store of one layer: event-major rows.
+struct DeviceLayer {
+    uint32_t n_union = 0;   // U: distinct events over the layer's ELTs
+    uint32_t n_cols = 0;    // E: ELTs of the layer
+    uint32_t width = 0;     // W = row_width_for(E) doubles (whole 32-byte chunks)
+    int group_override = 0; // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
+    uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
+    double *d_rows = nullptr;    // [(U+1) * W], row 0 zero
+    ScanTerms terms{};
+};
+
+struct ScanLaunch {
+    const uint64_t *offsets;  // [n+1], device
+    const uint32_t *ids;      // device, indexed by offsets[t] - offsets[0]
+    double *ylt;              // [n], device
+    uint64_t n_trials;
+    uint32_t catalogue_size;
+    uint32_t *err;            // device error word (bit 0: id out of range)
+};
+
+// scan.cu
+cudaError_t launch_scan(const DeviceLayer &L, const ScanLaunch &s, int sm_count,
+                        cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
+                            uint32_t catalogue_size, uint32_t *err, int sm_count,
+                            cudaStream_t stream, uint64_t *launches);
+
+// metrics.cu
+struct MetricsScratch {
+    void *d_buf = nullptr;
+    size_t bytes = 0;
+    int grid = 0;
+};
+cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
+                           double *pml_out, double *tvar_out, MetricsScratch &scratch,
+                           int sm_count, int device, cudaStream_t stream, uint64_t *launches);
+
+constexpr uint32_t kErrRange = 1u;
+constexpr uint32_t kErrOffsets = 2u;
+
+}  // namespace ara

@@ -1,0 +1,273 @@
+// scan.cu -- the YET scan kernel (Algorithm 1 lines 3-29 for one layer) for sm_100a.
+//
+// Decomposition: trial-per-group.  A group of G lanes (G = 4 for the paper's 15-16 ELT layers)
+// owns one trial; lane c of the group owns the CH consecutive 32-byte chunks
+// [c*CH, (c+1)*CH) of every event-major row, i.e. columns [4*CH*c, 4*CH*(c+1)), and keeps
+// those columns' financial terms in its own registers.  Per event:
+//   A2  all G lanes read the event id (256-bit loads of 8 ids, no L1 allocation, L2
+//       evict-first: the YET is streamed once),
+//   A3  map the catalogue id to a dense row (u32 map, L2-resident) and gather the row
+//       together: one 256-bit load per lane and chunk, the group covering whole 128-byte lines
+//       (measured 3x the event rate of one-lane-per-row gathers: profiles/README.md),
+//   A4  each lane applies the financial terms to its columns; the ELT sum of lines 11-13 runs
+//       as a chain through the group in column order (lane 0 adds its columns to +0 and
+//       passes the partial to lane 1 by shuffle, ...), so lo = ((0 + F_0) + F_1) + ... in the
+//       layer's ELT order, exactly the oracle's sequence,
+//   A5-A7 lane G-1 applies the occurrence terms, adds to the running sum S, applies the
+//       aggregate terms, differences against C_{d-1} and adds to lr,
+//   A8  lane G-1 writes lr to the YLT.
+// Every product / difference / sum is a separately rounded fp64 op (__dmul_rn, __dsub_rn,
+// __dadd_rn; the file is also built with -fmad=false), min/max are the oracle's compares.
+// The event loop is a rolled software pipeline: row(d+1) and map(d+2) are in flight while
+// event d is computed.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "ara_internal.h"
+
+namespace ara {
+namespace {
+
+struct Row4 {
+    double v[4];
+};
+
+__device__ __forceinline__ void load_row_chunk(const double *p, Row4 &r)
+{
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+        : "l"(p));
+}
+
+__device__ __forceinline__ void load_ids8(const uint32_t *p, uint32_t (&v)[8])
+{
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7])
+        : "l"(p));
+}
+
+__device__ __forceinline__ uint32_t load_id(const uint32_t *p)
+{
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t load_map(const uint32_t *p)
+{
+    uint32_t v;
+    asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// min(x, y) = (y < x ? y : x); max(x, 0) = (x < 0 ? 0 : x)   (the oracle's definitions)
+__device__ __forceinline__ double dmin(double x, double y) { return (y < x) ? y : x; }
+__device__ __forceinline__ double dmax0(double x) { return (x < 0.0) ? 0.0 : x; }
+
+__device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, uint32_t id,
+                                              uint32_t C, bool &bad)
+{
+    const bool ok = (id - 1u) < C;  // id in [1, C]
+    bad |= !ok;
+    return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
+}
+
+// Per-group event stream of one trial: ids arrive in 32-byte (8-id) vectors through a shifting
+// register queue, so the event loop stays rolled (no dynamic register indexing, no hoisting of
+// many row gathers).  All G lanes of a group read the same ids (one request per group).
+struct IdStream {
+    const uint32_t *p;  // next id to enqueue
+    uint64_t left;      // ids not yet enqueued
+    uint32_t q[8];      // queue, q[0] is the next id to hand out
+    uint32_t n;         // valid entries in q
+
+    __device__ __forceinline__ void refill()
+    {
+        if (left >= 8 && ((uintptr_t)p & 31u) == 0) {  // aligned: one 256-bit load
+            load_ids8(p, q);
+            p += 8;
+            left -= 8;
+            n = 8;
+        } else {  // unaligned head / short tail: scalar
+            q[0] = load_id(p);
+            ++p;
+            --left;
+            n = 1;
+        }
+    }
+    __device__ __forceinline__ uint32_t pop()
+    {
+        if (n == 0) refill();
+        const uint32_t v = q[0];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) q[i] = q[i + 1];
+        --n;
+        return v;
+    }
+};
+
+template <int G, int CH>
+__global__ void __launch_bounds__(256)
+    scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
+                const double *__restrict__ rows, const __grid_constant__ ScanTerms T)
+{
+    constexpr int W = 4 * G * CH;  // row width (doubles)
+    constexpr int NCOL = 4 * CH;   // columns per lane
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t c = lane % G;   // this lane's position in its group
+    const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - c));
+
+    double rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) {
+        rate[j] = T.rate[NCOL * c + j];
+        ret[j] = T.ret[NCOL * c + j];
+        lim[j] = T.lim[NCOL * c + j];
+    }
+    const double occ_ret = T.occ_ret, occ_lim = T.occ_lim;
+    const double agg_ret = T.agg_ret, agg_lim = T.agg_lim;
+    const double *__restrict__ my_rows = rows + NCOL * c;
+
+    const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
+    const uint64_t base = s.offsets[0];
+    bool bad = false;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; t < s.n_trials;
+         t += groups) {
+        const uint64_t beg = s.offsets[t] - base;
+        const uint64_t k = s.offsets[t + 1] - base - beg;
+        double S = 0.0, Cprev = 0.0, lr = 0.0;  // lines 19, 25 (C_0 = 0), 28
+        if (k != 0) {
+            IdStream ids{s.ids + beg, k, {}, 0};
+            uint32_t idx_nxt = map_index(map, ids.pop(), s.catalogue_size, bad);
+            uint32_t idx_aft = k > 1 ? map_index(map, ids.pop(), s.catalogue_size, bad) : 0u;
+            Row4 cur[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i)
+                load_row_chunk(my_rows + (size_t)idx_nxt * W + 4 * i, cur[i]);
+            idx_nxt = idx_aft;
+#pragma unroll 1
+            for (uint64_t d = 0; d < k; ++d) {
+                Row4 nxt[CH];
+                if (d + 1 < k) {
+#pragma unroll
+                    for (int i = 0; i < CH; ++i)
+                        load_row_chunk(my_rows + (size_t)idx_nxt * W + 4 * i, nxt[i]);
+                }
+                idx_aft = 0;
+                if (d + 2 < k) idx_aft = map_index(map, ids.pop(), s.catalogue_size, bad);
+
+                // A4, line 9 on this lane's columns: min(max(x*rate - ret, 0), lim)
+                double f[NCOL];
+#pragma unroll
+                for (int i = 0; i < CH; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = 4 * i + q;
+                        const double l = __dsub_rn(__dmul_rn(cur[i].v[q], rate[j]), ret[j]);
+                        f[j] = dmin(dmax0(l), lim[j]);
+                    }
+                // lines 11-13: lo = ((0 + F_0) + F_1) + ... through the group in column order
+                double part = 0.0;
+#pragma unroll
+                for (int j = 0; j < NCOL; ++j) part = __dadd_rn(part, f[j]);
+#pragma unroll
+                for (int h = 1; h < G; ++h) {
+                    double x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
+#pragma unroll
+                    for (int j = 0; j < NCOL; ++j) x = __dadd_rn(x, f[j]);
+                    part = x;  // valid in lane h after hop h
+                }
+                // A5-A7 (valid in lane G-1)
+                const double oc = dmin(dmax0(__dsub_rn(part, occ_ret)), occ_lim);  // line 16
+                S = __dadd_rn(S, oc);                                                // line 19
+                const double Cd = dmin(dmax0(__dsub_rn(S, agg_ret)), agg_lim);       // line 22
+                lr = __dadd_rn(lr, __dsub_rn(Cd, Cprev));                            // 25, 28
+                Cprev = Cd;
+#pragma unroll
+                for (int i = 0; i < CH; ++i) cur[i] = nxt[i];
+                idx_nxt = idx_aft;
+            }
+        }
+        if (c == G - 1) s.ylt[t] = lr;  // A8
+    }
+    if (bad) atomicOr(s.err, kErrRange);
+}
+
+// Device-side validation (ARA_RUN_VALIDATE): offsets non-decreasing, ids in [1, C].
+__global__ void validate_kernel(const uint64_t *__restrict__ offsets,
+                                const uint32_t *__restrict__ ids, uint64_t n_trials,
+                                uint32_t C, uint32_t *err)
+{
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t e = 0;
+    for (uint64_t t = tid; t < n_trials; t += stride)
+        if (offsets[t + 1] < offsets[t]) e |= kErrOffsets;
+    if (__syncthreads_or(e != 0)) {
+        if (threadIdx.x == 0) atomicOr(err, kErrOffsets);
+        return;
+    }
+    const uint64_t n_ev = offsets[n_trials] - offsets[0];
+    for (uint64_t i = tid; i < n_ev; i += stride)
+        if (ids[i] - 1u >= C) e |= kErrRange;
+    if (e) atomicOr(err, e);
+}
+
+template <int G, int CH>
+cudaError_t launch_gc(const DeviceLayer &L, const ScanLaunch &s, int sm_count, cudaStream_t stream)
+{
+    static int occ = 0;  // resident 256-thread blocks per SM for this instantiation
+    if (occ == 0) {
+        cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_kernel<G, CH>, 256, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    // Balanced single wave: every group gets ceil(n / groups) or one fewer trials, and the
+    // grid is a multiple of the SM count so every SM holds the same number of groups.
+    const uint64_t per_block = 256 / G;
+    const uint64_t groups_max = (uint64_t)sm_count * occ * per_block;
+    const uint64_t rounds = (s.n_trials + groups_max - 1) / groups_max;
+    const uint64_t groups = (s.n_trials + rounds - 1) / rounds;
+    uint64_t blocks = (groups + per_block - 1) / per_block;
+    if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
+    if (blocks > (uint64_t)sm_count * occ) blocks = (uint64_t)sm_count * occ;
+    scan_kernel<G, CH><<<(unsigned)blocks, 256, 0, stream>>>(s, L.d_map, L.d_rows, L.terms);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_scan(const DeviceLayer &L, const ScanLaunch &s, int sm_count,
+                        cudaStream_t stream, uint64_t *launches)
+{
+    if (s.n_trials == 0) return cudaSuccess;
+    ++*launches;
+    const ScanShape sh = scan_shape_for_width(L.width, L.group_override);
+    switch (sh.G * 16 + sh.CH) {
+        case 1 * 16 + 1: return launch_gc<1, 1>(L, s, sm_count, stream);
+        case 2 * 16 + 1: return launch_gc<2, 1>(L, s, sm_count, stream);
+        case 4 * 16 + 1: return launch_gc<4, 1>(L, s, sm_count, stream);
+        case 4 * 16 + 2: return launch_gc<4, 2>(L, s, sm_count, stream);
+        case 4 * 16 + 3: return launch_gc<4, 3>(L, s, sm_count, stream);
+        case 4 * 16 + 4: return launch_gc<4, 4>(L, s, sm_count, stream);
+        case 2 * 16 + 2: return launch_gc<2, 2>(L, s, sm_count, stream);  // W = 16 with G = 2
+        case 1 * 16 + 4: return launch_gc<1, 4>(L, s, sm_count, stream);  // W = 16 with G = 1
+        default: --*launches; return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
+                            uint32_t catalogue_size, uint32_t *err, int sm_count,
+                            cudaStream_t stream, uint64_t *launches)
+{
+    if (n_trials == 0) return cudaSuccess;
+    ++*launches;
+    validate_kernel<<<sm_count * 8, 256, 0, stream>>>(offsets, ids, n_trials, catalogue_size,
+                                                     err);
+    return cudaGetLastError();
+}
+
+}  // namespace ara

@@ -1,0 +1,337 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): every YLT entry bit-identical to the oracle
+(the kernel performs the oracle's fp64 operations in the oracle's order; -0 == +0), PML exact,
+TVaR within 1e-9 relative (its tail sum is reduced in a different order).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from tests._util import make_dataset
+
+torch = pytest.importorskip("torch")
+from paper_1308_2572_b200 import ara  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+P_RP = [1 - 1 / rp for rp in (10, 25, 50, 100, 250, 500, 1000)]
+
+
+@pytest.fixture(scope="module")
+def stream():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return torch.cuda.current_stream(torch.device(DEV))
+
+
+def to_dev(a: np.ndarray, kind: str):
+    if kind == "u64":
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(DEV).view(torch.uint64)
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).to(DEV).view(torch.uint32)
+
+
+def make_ctx(ds, stream):
+    ctx = ara.Context(0, stream)
+    ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    return ctx
+
+
+def gpu_ylt(ds, stream, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_VALIDATE, ctx=None, offsets=None,
+            events=None):
+    own = ctx is None
+    ctx = ctx or make_ctx(ds, stream)
+    off = ds.trial_offsets if offsets is None else offsets
+    ev = ds.events if events is None else events
+    n = off.shape[0] - 1
+    ylt = torch.full((ds.n_layers, n), float("nan"), dtype=torch.float64, device=DEV)
+    ctx.ara_run(to_dev(off, "u64"), to_dev(ev, "u32"), ylt, flags=flags)
+    out = ylt.cpu().numpy()
+    if own:
+        ctx.close()
+    return out
+
+
+def assert_bit_identical(got, want):
+    assert got.shape == want.shape
+    bad = np.flatnonzero(~((got == want) | (np.isnan(got) & np.isnan(want))))
+    assert bad.size == 0, (f"{bad.size} of {got.size} YLT entries differ; first at {bad[:5]}: "
+                           f"gpu {got.ravel()[bad[:5]]} oracle {want.ravel()[bad[:5]]}")
+
+
+# --------------------------------------------------------------------------- YLT parity
+@pytest.mark.parametrize("seed", [1308, 2572, 42])
+def test_tiny_bit_identical(stream, seed):
+    ds = datagen.generate(datagen.PRESETS["tiny"].replace(seed=seed))
+    assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds))
+
+
+def test_medium_shape_bit_identical(stream):
+    """configs[1] shape (C = 2M, 16 ELTs x 10k records, 1000 events/trial), 3000 trials: several
+    full waves of tiles, all 32-byte id chunks plus the per-lane pipeline at full depth."""
+    spec = datagen.PRESETS["medium"].replace(n_trials=3000)
+    ds = datagen.generate(spec)
+    assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds, n_threads=8))
+
+
+@pytest.mark.parametrize("n_elts", [1, 3, 4, 5, 8, 15, 16, 17, 32, 33, 64])
+def test_elts_per_layer_widths(stream, n_elts):
+    """Every row width class (W = 4..64; padded columns must be exactly neutral)."""
+    spec = datagen.PRESETS["tiny"].replace(n_elts=n_elts, elts_per_layer=n_elts, n_trials=400,
+                                           k_min=0, k_max=40, seed=7 + n_elts)
+    ds = datagen.generate(spec)
+    assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds))
+
+
+def test_ragged_and_misaligned(stream):
+    """Variable lengths (0..37 events, empty trials included), a YET slice whose offsets start
+    at a non-zero base and whose id pointer is not 32-byte aligned (head/tail paths)."""
+    spec = datagen.PRESETS["tiny"].replace(n_trials=3000, k_min=0, k_max=37, seed=99)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds)
+    assert_bit_identical(gpu_ylt(ds, stream), want)
+    for shift in (1, 3, 5, 7):
+        ev = np.concatenate([np.full(shift, 1, np.uint32), ds.events])
+        off = ds.trial_offsets + np.uint64(shift)
+        ctx = make_ctx(ds, stream)
+        n = ds.n_trials
+        ylt = torch.empty((1, n), dtype=torch.float64, device=DEV)
+        d_ev = to_dev(ev, "u32")
+        # pass a pointer to ev[shift:] with offsets based at `shift`: ids of trial t are
+        # d_ev[shift + off[t] - off[0] ...]
+        ctx.ara_run(to_dev(off, "u64"), d_ev[shift:], ylt, flags=ara.ARA_RUN_SYNC)
+        assert_bit_identical(ylt.cpu().numpy(), want)
+        ctx.close()
+
+
+def test_sharding_invariance(stream):
+    """Trial slices run separately and concatenated equal the whole run bit for bit (the
+    multi-GPU partition)."""
+    ds = datagen.generate(datagen.PRESETS["tiny"].replace(n_trials=2000, k_min=5, k_max=30))
+    full = gpu_ylt(ds, stream)
+    ctx = make_ctx(ds, stream)
+    parts = []
+    cuts = [0, 1, 333, 334, 1500, 2000]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        off = ds.trial_offsets[a:b + 1]
+        ev = ds.events[int(off[0]):int(off[-1])]
+        parts.append(gpu_ylt(ds, stream, ctx=ctx, offsets=off, events=ev))
+    ctx.close()
+    assert_bit_identical(np.concatenate(parts, axis=1), full)
+
+
+def test_multilayer_portfolio_shape(stream):
+    """configs[3] shape: 8 layers sharing 64 ELTs (each ELT in two layers), distinct terms."""
+    spec = datagen.PRESETS["portfolio"].replace(n_trials=600, k_min=100, k_max=300)
+    ds = datagen.generate(spec)
+    assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds, n_threads=8))
+
+
+def test_ylt_leading_dimension(stream):
+    spec = datagen.PRESETS["portfolio"].replace(n_trials=100, k_min=10, k_max=20, n_elts=16,
+                                                n_layers=3, elts_per_layer=8, layer_stride=4)
+    ds = datagen.generate(spec)
+    ctx = make_ctx(ds, stream)
+    ld = 131
+    ylt = torch.full((3, ld), -7.0, dtype=torch.float64, device=DEV)
+    ctx.ara_run(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, ylt_ld=ld,
+                flags=ara.ARA_RUN_SYNC)
+    got = ylt.cpu().numpy()
+    assert_bit_identical(got[:, :100], oracle.run_analysis(ds))
+    assert (got[:, 100:] == -7.0).all()  # nothing written past n in each row
+    ctx.close()
+
+
+def _adversarial_dataset():
+    """Hand-built cases where the order of fp64 operations decides the result."""
+    rng = np.random.default_rng(5)
+    cat = 64
+    elts = []
+    for j in range(5):
+        ids = rng.choice(np.arange(1, cat + 1), 40, replace=False)
+        ls = rng.uniform(0.1, 1e6, 40) * (10.0 ** rng.integers(-3, 4, 40))
+        fin = (1.0 + rng.uniform(-0.3, 0.3), float(rng.uniform(0, 1e4)),
+               math.inf if j % 2 else float(rng.uniform(1e4, 1e6)))
+        elts.append({"records": list(zip(ids.tolist(), ls.tolist())), "fin": fin})
+    trials = [list(rng.integers(1, cat + 1, rng.integers(0, 60))) for _ in range(400)]
+    trials += [[3] * 50, [], [1], list(range(1, cat + 1))]  # repeats, empty, all
+    return cat, elts, trials
+
+
+def test_adversarial_cancellation(stream):
+    """AggR set to (close to) trial sums S so that S - AggR cancels: the result depends on the
+    exact summation order; limits 0 and +inf; OccR equal to an event's combined loss."""
+    cat, elts, trials = _adversarial_dataset()
+    base = make_dataset(cat, elts, [{"elts": [0, 1, 2, 3, 4], "terms": (0, math.inf, 0, math.inf)}],
+                        trials)
+    S = oracle.run_analysis(base)[0]  # identity aggregate terms: lr ~ S
+    lo_single = oracle.run_analysis(make_dataset(cat, elts, [{"elts": [0, 1, 2, 3, 4],
+                                                              "terms": (0, math.inf, 0, math.inf)}],
+                                                 [[e] for e in range(1, cat + 1)]))[0]
+    cases = []
+    for t in (0, 5, 17, 123):
+        cases.append((0.0, math.inf, float(S[t]), math.inf))
+        cases.append((0.0, math.inf, float(S[t]), 1.0))
+        cases.append((0.0, math.inf, float(np.nextafter(S[t], 0)), math.inf))
+    cases += [(float(lo_single[2]), math.inf, 0.0, math.inf), (0.0, 0.0, 0.0, math.inf),
+              (10.0, 1e5, 0.0, 0.0), (1e9, math.inf, 0.0, math.inf)]
+    layers = [{"elts": [0, 1, 2, 3, 4], "terms": c} for c in cases]
+    ds = make_dataset(cat, elts, layers, trials)
+    want = oracle.run_analysis(ds)
+    got = gpu_ylt(ds, stream)
+    assert_bit_identical(got, want)
+    assert (want[0] == 0).any()  # a trial whose S equals AggR pays exactly 0
+
+
+def test_absent_events_only(stream):
+    spec = datagen.PRESETS["tiny"].replace(hit=0.0, catalogue_size=100_000, n_trials=500)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds)
+    assert_bit_identical(gpu_ylt(ds, stream), want)
+
+
+# --------------------------------------------------------------------------- store (A1)
+@pytest.mark.parametrize("preset", ["tiny", "medium"])
+def test_store_round_trip(stream, preset):
+    """rows[map[e]][c] == DAT_c[e] for every catalogue id e and layer ELT c,
+    bit for bit; map[0] = 0 and row 0 is zero."""
+    ds = datagen.generate(datagen.PRESETS[preset], with_yet=False)
+    ctx = make_ctx(ds, stream)
+    m, rows = ctx.ara_export_store(0, ds.catalogue_size)
+    E = int(ds.elt_offsets[1])
+    U, W = ctx.ara_layer_store_shape(0)
+    assert W == (E + 3) // 4 * 4 and m[0] == 0 and (rows[0] == 0).all()
+    assert (rows[:, E:] == 0).all()
+    for c in range(E):
+        j = int(ds.elt_index[c])
+        a, b = int(ds.rec_offsets[j]), int(ds.rec_offsets[j + 1])
+        dat = oracle.build_dat(ds.catalogue_size, ds.rec_event_ids[a:b], ds.rec_losses[a:b])
+        assert np.array_equal(rows[m, c].view(np.uint64), dat.view(np.uint64))
+    assert U == len(np.unique(ds.rec_event_ids))
+    ctx.close()
+
+
+# --------------------------------------------------------------------------- host path
+def test_run_host_matches(stream):
+    spec = datagen.PRESETS["portfolio"].replace(n_trials=700, k_min=50, k_max=150, n_layers=2)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds, n_threads=8)
+    ctx = make_ctx(ds, stream)
+    h = np.empty((2, 700))
+    ctx.ara_run_host(ds.trial_offsets, ds.events, h)
+    assert_bit_identical(h, want)
+    pinned_ev = torch.from_numpy(ds.events.view(np.int32)).pin_memory()
+    h2 = np.zeros((2, 710))
+    ctx.ara_run_host(ds.trial_offsets, pinned_ev.numpy().view(np.uint32), h2, ylt_ld=710)
+    assert_bit_identical(h2[:, :700], want)
+    ctx.close()
+
+
+# --------------------------------------------------------------------------- metrics (A9)
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 100_003])
+def test_metrics_parity(stream, n):
+    rng = np.random.default_rng(n)
+    v = np.round(rng.exponential(1e6, n), 2) * (rng.random(n) < 0.7)
+    ps = P_RP + [0.5, 0.999999]
+    ctx = ara.Context(0, stream)
+    pml, tvar = ctx.ara_metrics(torch.from_numpy(v).to(DEV), ps)
+    opml, otvar = oracle.metrics(v, ps)
+    assert np.array_equal(pml, opml)
+    assert np.allclose(tvar, otvar, rtol=1e-9, atol=0)
+    hp, ht = ctx.ara_metrics_host(v, ps)
+    assert np.array_equal(hp, opml) and np.allclose(ht, otvar, rtol=1e-9, atol=0)
+    ctx.close()
+
+
+def test_metrics_ties_constant_and_zeros(stream):
+    ctx = ara.Context(0, stream)
+    for v in (np.zeros(1000), np.full(513, 3.25), np.repeat([0.0, 1.0, 2.0, 2.0, 5.0], 200),
+              np.concatenate([np.zeros(10), -np.zeros(10), np.ones(3)])):
+        pml, tvar = ctx.ara_metrics(torch.from_numpy(v).to(DEV), P_RP)
+        opml, otvar = oracle.metrics(v, P_RP)
+        assert np.array_equal(pml, opml)
+        assert np.allclose(tvar, otvar, rtol=1e-9, atol=0)
+    ctx.close()
+
+
+def test_metrics_on_ylt(stream):
+    ds = datagen.generate(datagen.PRESETS["medium"].replace(n_trials=4000, k_min=200, k_max=200))
+    ctx = make_ctx(ds, stream)
+    ylt = torch.empty((1, ds.n_trials), dtype=torch.float64, device=DEV)
+    ctx.ara_run(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt,
+                flags=ara.ARA_RUN_SYNC)
+    pml, tvar = ctx.ara_metrics(ylt[0], P_RP)
+    want = oracle.run_analysis(ds, n_threads=8)[0]
+    opml, otvar = oracle.metrics(want, P_RP)
+    assert np.array_equal(pml, opml)
+    assert np.allclose(tvar, otvar, rtol=1e-9, atol=0)
+    ctx.close()
+
+
+# --------------------------------------------------------------------------- errors
+def test_errors(stream):
+    ds = datagen.generate(datagen.PRESETS["tiny"])
+    ctx = ara.Context(0, stream)
+    ylt = torch.empty((1, ds.n_trials), dtype=torch.float64, device=DEV)
+    off, ev = to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32")
+    with pytest.raises(ara.AraError, match="ARA_ERR_STATE"):
+        ctx.ara_run(off, ev, ylt)
+    with pytest.raises(ara.AraError, match="ARA_ERR_STATE"):
+        ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    bad_ids = ds.rec_event_ids.copy(); bad_ids[5] = ds.catalogue_size + 1
+    with pytest.raises(ara.AraError, match="ARA_ERR_RANGE"):
+        ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, bad_ids, ds.rec_losses, ds.fin)
+    dup = ds.rec_event_ids.copy(); dup[1] = dup[0]
+    with pytest.raises(ara.AraError, match="ARA_ERR_VALIDATION"):
+        ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, dup, ds.rec_losses, ds.fin)
+    fin = ds.fin.copy(); fin[0, 0] = 0.0
+    with pytest.raises(ara.AraError, match="ARA_ERR_VALIDATION"):
+        ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, fin)
+    ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
+    lt = ds.layer_terms.copy(); lt[0, 2] = -1.0
+    with pytest.raises(ara.AraError, match="ARA_ERR_VALIDATION"):
+        ctx.ara_set_layers(lt, ds.elt_offsets, ds.elt_index)
+    with pytest.raises(ara.AraError, match="ARA_ERR_VALIDATION"):
+        ctx.ara_set_layers(ds.layer_terms, np.array([0, 2], np.uint32), np.array([0, 0], np.uint32))
+    with pytest.raises(ara.AraError, match="ARA_ERR_UNSUPPORTED"):
+        ctx.ara_set_layers(ds.layer_terms, np.array([0, 65], np.uint32), np.zeros(65, np.uint32))
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    bad = ds.events.copy(); bad[17] = 0
+    with pytest.raises(ara.AraError, match="ARA_ERR_RANGE"):
+        ctx.ara_run(off, to_dev(bad, "u32"), ylt, flags=ara.ARA_RUN_VALIDATE)
+    bad[17] = ds.catalogue_size + 5
+    ctx.ara_run(off, to_dev(bad, "u32"), ylt)  # asynchronous: error deferred ...
+    with pytest.raises(ara.AraError, match="ARA_ERR_RANGE"):
+        ctx.ara_synchronize()                   # ... and reported here
+    ctx.ara_synchronize()                       # and cleared
+    dec = ds.trial_offsets.copy(); dec[3], dec[4] = dec[4], dec[3]
+    with pytest.raises(ara.AraError, match="ARA_ERR_VALIDATION"):
+        ctx.ara_run(to_dev(dec, "u64"), ev, ylt, flags=ara.ARA_RUN_VALIDATE)
+    with pytest.raises(ara.AraError, match="ARA_ERR_EMPTY"):
+        ctx.ara_metrics(torch.empty(0, dtype=torch.float64, device=DEV), [0.5])
+    with pytest.raises(ara.AraError, match="ARA_ERR_ARG"):
+        ctx.ara_metrics(ylt[0], [1.0])
+    n0 = ctx.kernel_launches
+    ctx.ara_run(off, ev, ylt, flags=ara.ARA_RUN_SYNC)
+    assert ctx.kernel_launches == n0 + 1
+    ctx.close()
+
+
+# --------------------------------------------------------------------------- full size
+def test_headline_size_sampled(stream):
+    """configs[2] at full size (1M trials x 1000 events, E = 16, C = 2M) in the launch
+    configuration bench.py times: 2,000 sampled trials bit-identical to the oracle, and the
+    bounds 0 <= lr <= AggL on every entry (a property that holds at any size)."""
+    spec = datagen.PRESETS["headline"]
+    ds = datagen.generate(spec)
+    got = gpu_ylt(ds, stream, flags=ara.ARA_RUN_SYNC)
+    assert not np.isnan(got).any()
+    aggL = ds.layer_terms[0, 3]
+    assert (got >= 0).all() and (got <= aggL).all()
+    sel = np.random.default_rng(1).choice(ds.n_trials, 2000, replace=False).astype(np.uint64)
+    sel = np.concatenate([sel, np.array([0, ds.n_trials - 1], np.uint64)])
+    want = oracle.run_analysis(ds, selection=sel, n_threads=8)
+    assert_bit_identical(got[:, sel.astype(np.int64)], want)
