@@ -352,6 +352,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
             L.n_cols = E;
             L.width = W;
             if (const char *g = getenv("ARA_SCAN_GROUP")) L.group_override = atoi(g);
+            if (const char *m = getenv("ARA_SCAN_MINB")) L.min_blocks = atoi(m);
             // union of the layer's events, ascending id -> dense rows 1..U
             std::vector<uint32_t> uni;
             for (uint32_t c = 0; c < E; ++c) {

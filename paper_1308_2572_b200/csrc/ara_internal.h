@@ -26,8 +26,10 @@ struct ScanTerms {
 };
 
 // Scan decomposition for a row width: G lanes per trial, each owning CH 32-byte chunks
-// (4 doubles each), W = 4 * G * CH.  The paper's 15-16 ELT layers give W = 16, G = 4: one
-// 128-byte row per group, one 256-bit load per lane.
+// (4 doubles each), W = 4 * G * CH.  The paper's 15-16 ELT layers give W = 16 and G = 2: a
+// 128-byte row is gathered by two lanes (two 256-bit loads each) and the ELT-sum chain has one
+// shuffle hop.  Measured on B200 at the headline (profiles/r1_tune_scan.jsonl): G = 2 12.9 ms,
+// G = 4 17.2 ms (3 hops: issue-bound), G = 1 22.9 ms (uncoalesced gathers: L1-request-bound).
 struct ScanShape {
     int G, CH;
 };
@@ -38,7 +40,7 @@ inline uint32_t row_width_for(uint32_t E)
     const uint32_t nc = (E + 3) / 4;  // 32-byte chunks needed
     if (nc <= 1) return 4;
     if (nc == 2) return 8;
-    return 16 * ((nc + 3) / 4);       // G = 4, CH = ceil(nc / 4)
+    return 16 * ((nc + 3) / 4);       // multiples of 16 doubles
 }
 
 // Decomposition for a store of width W; override (1, 2 or 4) selects G for W = 16 only.
@@ -46,7 +48,10 @@ inline ScanShape scan_shape_for_width(uint32_t W, int override_g)
 {
     if (W == 4) return {1, 1};
     if (W == 8) return {2, 1};
-    if (W == 16 && (override_g == 1 || override_g == 2)) return {override_g, 4 / override_g};
+    if (W == 16) {
+        if (override_g == 1 || override_g == 4) return {override_g, 4 / override_g};
+        return {2, 2};
+    }
     return {4, (int)(W / 16)};
 }
 
@@ -56,6 +61,7 @@ struct DeviceLayer {
     uint32_t n_cols = 0;    // E: ELTs of the layer
     uint32_t width = 0;     // W = row_width_for(E) doubles (whole 32-byte chunks)
     int group_override = 0; // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
+    int min_blocks = 0;     // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     double *d_rows = nullptr;    // [(U+1) * W], row 0 zero
     ScanTerms terms{};

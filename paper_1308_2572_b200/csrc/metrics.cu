@@ -102,19 +102,22 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
         __syncthreads();
     }
 
-    // Tail sums over this block's contiguous chunk, per probability, in a fixed order.
+    // Tail sums over this block's contiguous chunk, per probability, in a fixed order.  The sum
+    // is of (v - PML) >= 0, so TVaR = PML + mean(v - PML) >= PML holds exactly and the
+    // rounding error scales with the tail's spread, not its level.
     const uint64_t chunk = (P.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < P.n ? lo + chunk : P.n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t i = 0; i < n_p; ++i) {
         const uint64_t q = s_prefix[i];
+        const double qv = from_key(q);
         double s = 0.0;
         unsigned long long c = 0;
         for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
             const double x = P.v[e];
             if (to_key(x) >= q) {
-                s += x;
+                s += x - qv;
                 ++c;
             }
         }
@@ -148,8 +151,9 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
             s += __ldcg(P.part_sum + (size_t)b * ARA_MAX_P + i);
             c += __ldcg(P.part_cnt + (size_t)b * ARA_MAX_P + i);
         }
-        P.out[i] = from_key(s_prefix[i]);
-        P.out[ARA_MAX_P + i] = s / (double)c;
+        const double q = from_key(s_prefix[i]);
+        P.out[i] = q;
+        P.out[ARA_MAX_P + i] = q + s / (double)c;
     }
 }
 

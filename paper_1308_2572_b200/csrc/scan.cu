@@ -1,6 +1,6 @@
 // scan.cu -- the YET scan kernel (Algorithm 1 lines 3-29 for one layer) for sm_100a.
 //
-// Decomposition: trial-per-group.  A group of G lanes (G = 4 for the paper's 15-16 ELT layers)
+// Decomposition: trial-per-group.  A group of G lanes (G = 2 for the paper's 15-16 ELT layers)
 // owns one trial; lane c of the group owns the CH consecutive 32-byte chunks
 // [c*CH, (c+1)*CH) of every event-major row, i.e. columns [4*CH*c, 4*CH*(c+1)), and keeps
 // those columns' financial terms in its own registers.  Per event:
@@ -28,6 +28,8 @@
 
 namespace ara {
 namespace {
+
+constexpr int kScanThreads = 128;  // 4 warps: fine occupancy steps for 80-170 registers
 
 struct Row4 {
     double v[4];
@@ -74,42 +76,64 @@ __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, 
     return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
 }
 
-// Per-group event stream of one trial: ids arrive in 32-byte (8-id) vectors through a shifting
-// register queue, so the event loop stays rolled (no dynamic register indexing, no hoisting of
-// many row gathers).  All G lanes of a group read the same ids (one request per group).
-struct IdStream {
-    const uint32_t *p;  // next id to enqueue
-    uint64_t left;      // ids not yet enqueued
-    uint32_t q[8];      // queue, q[0] is the next id to hand out
-    uint32_t n;         // valid entries in q
+// The row gather of event j+1 is issued while event j is computed.  `pin` gives the row index a
+// true data dependency on the running sum of the previous event (min with 2^32 - 1 - signbit(S),
+// which is 2^32 - 1 because S >= +0 and idx <= U < 2^32 - 1, so the value is unchanged): without
+// it ptxas hoists all eight gathers of an unrolled chunk and runs out of registers.
+__device__ __forceinline__ uint32_t pin(uint32_t idx, double S)
+{
+    const uint32_t sbit = (uint32_t)__double2hiint(S) >> 31;
+    return min(idx, 0xffffffffu - sbit);
+}
 
-    __device__ __forceinline__ void refill()
-    {
-        if (left >= 8 && ((uintptr_t)p & 31u) == 0) {  // aligned: one 256-bit load
-            load_ids8(p, q);
-            p += 8;
-            left -= 8;
-            n = 8;
-        } else {  // unaligned head / short tail: scalar
-            q[0] = load_id(p);
-            ++p;
-            --left;
-            n = 1;
-        }
-    }
-    __device__ __forceinline__ uint32_t pop()
-    {
-        if (n == 0) refill();
-        const uint32_t v = q[0];
-#pragma unroll
-        for (int i = 0; i < 7; ++i) q[i] = q[i + 1];
-        --n;
-        return v;
-    }
-};
-
+// A2-A8 for one event with its row chunks in r[] (see the file comment).
 template <int G, int CH>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&rate)[4 * CH],
+                                           const double (&ret)[4 * CH],
+                                           const double (&lim)[4 * CH], uint32_t gmask,
+                                           double occ_ret, double occ_lim, double agg_ret,
+                                           double agg_lim, double &S, double &Cprev, double &lr)
+{
+    constexpr int NCOL = 4 * CH;
+    // A4, line 9 on this lane's columns: min(max(x*rate - ret, 0), lim)
+    double f[NCOL];
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = 4 * i + q;
+            const double l = __dsub_rn(__dmul_rn(r[i].v[q], rate[j]), ret[j]);
+            f[j] = dmin(dmax0(l), lim[j]);
+        }
+    // lines 11-13: lo = ((0 + F_0) + F_1) + ... through the group in column order
+    double part = 0.0;
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) part = __dadd_rn(part, f[j]);
+#pragma unroll
+    for (int h = 1; h < G; ++h) {
+        double x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) x = __dadd_rn(x, f[j]);
+        part = x;  // valid in lane h after hop h
+    }
+    // A5-A7 (valid in lane G-1)
+    const double oc = dmin(dmax0(__dsub_rn(part, occ_ret)), occ_lim);  // line 16
+    S = __dadd_rn(S, oc);                                                // line 19
+    const double Cd = dmin(dmax0(__dsub_rn(S, agg_ret)), agg_lim);       // line 22
+    lr = __dadd_rn(lr, __dsub_rn(Cd, Cprev));                            // lines 25, 28
+    Cprev = Cd;
+}
+
+template <int CH, int W>
+__device__ __forceinline__ void gather(const double *__restrict__ my_rows, uint32_t idx,
+                                       Row4 (&r)[CH])
+{
+#pragma unroll
+    for (int i = 0; i < CH; ++i) load_row_chunk(my_rows + (size_t)idx * W + 4 * i, r[i]);
+}
+
+template <int G, int CH, int MINB>
+__global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                 const double *__restrict__ rows, const __grid_constant__ ScanTerms T)
 {
@@ -129,6 +153,7 @@ __global__ void __launch_bounds__(256)
     const double occ_ret = T.occ_ret, occ_lim = T.occ_lim;
     const double agg_ret = T.agg_ret, agg_lim = T.agg_lim;
     const double *__restrict__ my_rows = rows + NCOL * c;
+    const uint32_t C = s.catalogue_size;
 
     const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
     const uint64_t base = s.offsets[0];
@@ -137,58 +162,63 @@ __global__ void __launch_bounds__(256)
          t += groups) {
         const uint64_t beg = s.offsets[t] - base;
         const uint64_t k = s.offsets[t + 1] - base - beg;
+        const uint32_t *ev = s.ids + beg;
+        const uint32_t *const ev_end = ev + k;
         double S = 0.0, Cprev = 0.0, lr = 0.0;  // lines 19, 25 (C_0 = 0), 28
-        if (k != 0) {
-            IdStream ids{s.ids + beg, k, {}, 0};
-            uint32_t idx_nxt = map_index(map, ids.pop(), s.catalogue_size, bad);
-            uint32_t idx_aft = k > 1 ? map_index(map, ids.pop(), s.catalogue_size, bad) : 0u;
-            Row4 cur[CH];
-#pragma unroll
-            for (int i = 0; i < CH; ++i)
-                load_row_chunk(my_rows + (size_t)idx_nxt * W + 4 * i, cur[i]);
-            idx_nxt = idx_aft;
-#pragma unroll 1
-            for (uint64_t d = 0; d < k; ++d) {
-                Row4 nxt[CH];
-                if (d + 1 < k) {
-#pragma unroll
-                    for (int i = 0; i < CH; ++i)
-                        load_row_chunk(my_rows + (size_t)idx_nxt * W + 4 * i, nxt[i]);
-                }
-                idx_aft = 0;
-                if (d + 2 < k) idx_aft = map_index(map, ids.pop(), s.catalogue_size, bad);
 
-                // A4, line 9 on this lane's columns: min(max(x*rate - ret, 0), lim)
-                double f[NCOL];
+        // head: single events until the id pointer is 32-byte aligned
+        while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
+            Row4 r[CH];
+            gather<CH, W>(my_rows, map_index(map, load_id(ev), C, bad), r);
+            event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
+                              Cprev, lr);
+            ++ev;
+        }
+        // body: chunks of 8 events.  Pipeline per group: the ids of chunk i+1 are in flight
+        // during chunk i (one 32-byte load per chunk), the map lookup of event j+2 and the row
+        // gather of event j+1 are in flight while event j is computed.
+        const uint64_t n_chunks = (uint64_t)(ev_end - ev) / 8;
+        if (n_chunks) {
+            uint32_t id_c[8], id_n[8];
+            load_ids8(ev, id_c);
+            if (n_chunks > 1) load_ids8(ev + 8, id_n);
+            uint32_t idx0 = map_index(map, id_c[0], C, bad);
+            uint32_t idx1 = map_index(map, id_c[1], C, bad);
+            Row4 ra[CH];
+            gather<CH, W>(my_rows, idx0, ra);
+#pragma unroll 1
+            for (uint64_t i = 0; i < n_chunks; ++i) {
+                const bool more = i + 1 < n_chunks;
 #pragma unroll
-                for (int i = 0; i < CH; ++i)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int j = 4 * i + q;
-                        const double l = __dsub_rn(__dmul_rn(cur[i].v[q], rate[j]), ret[j]);
-                        f[j] = dmin(dmax0(l), lim[j]);
-                    }
-                // lines 11-13: lo = ((0 + F_0) + F_1) + ... through the group in column order
-                double part = 0.0;
-#pragma unroll
-                for (int j = 0; j < NCOL; ++j) part = __dadd_rn(part, f[j]);
-#pragma unroll
-                for (int h = 1; h < G; ++h) {
-                    double x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
-#pragma unroll
-                    for (int j = 0; j < NCOL; ++j) x = __dadd_rn(x, f[j]);
-                    part = x;  // valid in lane h after hop h
+                for (int j = 0; j < 8; j += 2) {
+                    // events j (in ra) and j+1: lookups of j+2, j+3 and gathers of j+1, j+2
+                    uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
+                    uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
+                    const bool ok2 = j + 2 < 8 || more;
+                    uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
+                    Row4 rb[CH];
+                    gather<CH, W>(my_rows, pin(idx1, S), rb);
+                    event_step<G, CH>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
+                                      agg_lim, S, Cprev, lr);
+                    uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
+                    gather<CH, W>(my_rows, pin(idx2, S), ra);  // event j+2 (zero row past end)
+                    event_step<G, CH>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
+                                      agg_lim, S, Cprev, lr);
+                    idx1 = idx3;
                 }
-                // A5-A7 (valid in lane G-1)
-                const double oc = dmin(dmax0(__dsub_rn(part, occ_ret)), occ_lim);  // line 16
-                S = __dadd_rn(S, oc);                                                // line 19
-                const double Cd = dmin(dmax0(__dsub_rn(S, agg_ret)), agg_lim);       // line 22
-                lr = __dadd_rn(lr, __dsub_rn(Cd, Cprev));                            // 25, 28
-                Cprev = Cd;
 #pragma unroll
-                for (int i = 0; i < CH; ++i) cur[i] = nxt[i];
-                idx_nxt = idx_aft;
+                for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
+                if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
             }
+            ev += 8 * n_chunks;
+        }
+        // tail: remaining events one by one
+        while (ev < ev_end) {
+            Row4 r[CH];
+            gather<CH, W>(my_rows, map_index(map, load_id(ev), C, bad), r);
+            event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
+                              Cprev, lr);
+            ++ev;
         }
         if (c == G - 1) s.ylt[t] = lr;  // A8
     }
@@ -215,26 +245,26 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
     if (e) atomicOr(err, e);
 }
 
-template <int G, int CH>
+template <int G, int CH, int MINB = 1>
 cudaError_t launch_gc(const DeviceLayer &L, const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
-    static int occ = 0;  // resident 256-thread blocks per SM for this instantiation
+    static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
-        cudaError_t e =
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, scan_kernel<G, CH>, 256, 0);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, scan_kernel<G, CH, MINB>, kScanThreads, 0);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
     // Balanced single wave: every group gets ceil(n / groups) or one fewer trials, and the
     // grid is a multiple of the SM count so every SM holds the same number of groups.
-    const uint64_t per_block = 256 / G;
+    const uint64_t per_block = kScanThreads / G;
     const uint64_t groups_max = (uint64_t)sm_count * occ * per_block;
     const uint64_t rounds = (s.n_trials + groups_max - 1) / groups_max;
     const uint64_t groups = (s.n_trials + rounds - 1) / rounds;
     uint64_t blocks = (groups + per_block - 1) / per_block;
     if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
     if (blocks > (uint64_t)sm_count * occ) blocks = (uint64_t)sm_count * occ;
-    scan_kernel<G, CH><<<(unsigned)blocks, 256, 0, stream>>>(s, L.d_map, L.d_rows, L.terms);
+    scan_kernel<G, CH, MINB><<<(unsigned)blocks, kScanThreads, 0, stream>>>(s, L.d_map, L.d_rows, L.terms);
     return cudaGetLastError();
 }
 
@@ -249,11 +279,21 @@ cudaError_t launch_scan(const DeviceLayer &L, const ScanLaunch &s, int sm_count,
     switch (sh.G * 16 + sh.CH) {
         case 1 * 16 + 1: return launch_gc<1, 1>(L, s, sm_count, stream);
         case 2 * 16 + 1: return launch_gc<2, 1>(L, s, sm_count, stream);
-        case 4 * 16 + 1: return launch_gc<4, 1>(L, s, sm_count, stream);
+        case 4 * 16 + 1:  // W = 16 with G = 4 (tuning)
+            switch (L.min_blocks) {
+                case 5: return launch_gc<4, 1, 5>(L, s, sm_count, stream);
+                case 6: return launch_gc<4, 1, 6>(L, s, sm_count, stream);
+                default: return launch_gc<4, 1>(L, s, sm_count, stream);
+            }
         case 4 * 16 + 2: return launch_gc<4, 2>(L, s, sm_count, stream);
         case 4 * 16 + 3: return launch_gc<4, 3>(L, s, sm_count, stream);
         case 4 * 16 + 4: return launch_gc<4, 4>(L, s, sm_count, stream);
-        case 2 * 16 + 2: return launch_gc<2, 2>(L, s, sm_count, stream);  // W = 16 with G = 2
+        case 2 * 16 + 2:  // W = 16 (default)
+            switch (L.min_blocks) {
+                case 4: return launch_gc<2, 2, 4>(L, s, sm_count, stream);
+                case 5: return launch_gc<2, 2, 5>(L, s, sm_count, stream);
+                default: return launch_gc<2, 2>(L, s, sm_count, stream);
+            }
         case 1 * 16 + 4: return launch_gc<1, 4>(L, s, sm_count, stream);  // W = 16 with G = 1
         default: --*launches; return cudaErrorInvalidValue;
     }

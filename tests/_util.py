@@ -88,7 +88,7 @@ def make_dataset(catalogue_size: int, elts: List[dict], layers: List[dict],
     for t in trials:
         ev.extend(t); to.append(len(ev))
     return types.SimpleNamespace(
-        catalogue_size=catalogue_size,
+        catalogue_size=catalogue_size, n_layers=len(layers), n_trials=len(trials),
         rec_offsets=np.array(rec_off, dtype=np.uint64),
         rec_event_ids=np.array(ids, dtype=np.uint32),
         rec_losses=np.array(losses, dtype=np.float64),
