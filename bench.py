@@ -308,7 +308,7 @@ def main():
         try:
             pj = json.load(open(prof))
             if pj.get("config") == spec.name and pj.get("n_trials") == n_loc:
-                traffic = pj.get("dram_bytes_per_launch")
+                traffic = pj.get("dram_bytes_per_launch") * L  # one launch per layer
         except Exception:
             pass
 
@@ -364,7 +364,8 @@ def main():
                        "return_periods": list(RETURN_PERIODS)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "scan_kernel<4,1> (ara_run)", "kernel_ms": scan_ms,
+                         "kernel": f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})",
+                         "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                          "bytes_model": "n*k*(4 + 8E) + 8n + 8(n+1) per layer"},
             "gpu_launches": launches,
