@@ -299,7 +299,9 @@ def main():
     # roofline of the dominant kernel (the scan): algorithmic bytes per launch (DESIGN.md
     # "Roofline"): per layer n*k*(4 + 8E) + n*8 (YLT) + (n+1)*8 (offsets); per rank.
     E = spec.elts_per_layer
-    bytes_alg = (n_ev * (4 + 8 * E) + n_loc * 8 + (n_loc + 1) * 8) * L
+    # one fused launch covers all layers: the id stream and offsets are read once, every layer's
+    # E-wide fp64 row segment is gathered per event, every layer's YLT entry is written
+    bytes_alg = n_ev * (4 + 8 * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
     peak, peak_src = measured_peak()
     achieved = bytes_alg / (scan_ms * 1e-3) / 1e9
     traffic = None
@@ -308,7 +310,7 @@ def main():
         try:
             pj = json.load(open(prof))
             if pj.get("config") == spec.name and pj.get("n_trials") == n_loc:
-                traffic = pj.get("dram_bytes_per_launch") * L  # one launch per layer
+                traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             pass
 
@@ -367,7 +369,8 @@ def main():
                          "kernel": f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})",
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
-                         "bytes_model": "n*k*(4 + 8E) + 8n + 8(n+1) per layer"},
+                         "bytes_model": "n*k*(4 + 8*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
+                                        "segment per event, YLT, offsets (north-star accounting)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,

@@ -34,7 +34,7 @@ struct ara_ctx {
     std::vector<double> rec_losses;
     std::vector<ara_fin_terms> fin;
 
-    std::vector<ara::DeviceLayer> layers;
+    ara::DeviceStore store;  // all layers (valid when have_layers)
     uint64_t store_bytes = 0;
 
     uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
@@ -101,11 +101,10 @@ bool limit_ok(double x) { return !isnan(x) && x >= 0.0; }  // +inf allowed
 
 void free_layers(ara_ctx *ctx)
 {
-    for (auto &L : ctx->layers) {
-        cudaFree(L.d_map);
-        cudaFree(L.d_rows);
-    }
-    ctx->layers.clear();
+    cudaFree(ctx->store.d_map);
+    cudaFree(ctx->store.d_rows);
+    cudaFree(ctx->store.d_terms);
+    ctx->store = ara::DeviceStore();
     ctx->store_bytes = 0;
     ctx->have_layers = false;
 }
@@ -152,15 +151,14 @@ ara_status check_device_error(ara_ctx *ctx)
     return ARA_OK;
 }
 
+// One scan launch covers every layer (layer-fused pass: one id read and one map lookup per
+// event serve all layers).
 ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const uint32_t *d_ids,
                          double *d_ylt, uint64_t ld)
 {
-    for (size_t l = 0; l < ctx->layers.size(); ++l) {
-        ara::ScanLaunch s{d_off, d_ids, d_ylt + l * ld, n, ctx->C, ctx->d_err};
-        cudaError_t e = ara::launch_scan(ctx->layers[l], s, ctx->sm_count, ctx->stream,
-                                         &ctx->launches);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
-    }
+    ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err};
+    cudaError_t e = ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
 }
 
@@ -342,65 +340,74 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         free_layers(ctx);
 
+        // A1: union of all layers' events (ascending id -> dense rows 1..U), one shared map, and
+        // event-major rows holding each layer's columns back to back (layer l at l * W).
         const uint32_t C = ctx->C;
-        std::vector<uint32_t> map((size_t)C + 1);
-        std::vector<uint32_t> seen((size_t)C + 1, 0);
+        ara::DeviceStore &st = ctx->store;
+        st.n_layers = n_layers;
+        uint32_t maxE = 0;
         for (uint32_t l = 0; l < n_layers; ++l) {
-            ara::DeviceLayer L;
-            const uint32_t E = elt_offsets[l + 1] - elt_offsets[l];
-            const uint32_t W = ara::row_width_for(E);
-            L.n_cols = E;
-            L.width = W;
-            if (const char *g = getenv("ARA_SCAN_GROUP")) L.group_override = atoi(g);
-            if (const char *m = getenv("ARA_SCAN_MINB")) L.min_blocks = atoi(m);
-            // union of the layer's events, ascending id -> dense rows 1..U
-            std::vector<uint32_t> uni;
-            for (uint32_t c = 0; c < E; ++c) {
-                const uint32_t j = elt_index[elt_offsets[l] + c];
-                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r) {
-                    const uint32_t id = ctx->rec_ids[r];
-                    if (seen[id] != l + 1) {
-                        seen[id] = l + 1;
-                        uni.push_back(id);
-                    }
+            st.n_cols.push_back(elt_offsets[l + 1] - elt_offsets[l]);
+            maxE = std::max(maxE, st.n_cols.back());
+        }
+        const uint32_t W = ara::row_width_for(maxE);
+        st.width = W;
+        if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
+        if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
+        std::vector<uint32_t> map((size_t)C + 1, 0u);
+        std::vector<uint32_t> uni;
+        for (uint32_t c = elt_offsets[0]; c < elt_offsets[n_layers]; ++c) {
+            const uint32_t j = elt_index[c];
+            for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r) {
+                const uint32_t id = ctx->rec_ids[r];
+                if (!map[id]) {
+                    map[id] = 1;
+                    uni.push_back(id);
                 }
             }
-            std::sort(uni.begin(), uni.end());
-            L.n_union = (uint32_t)uni.size();
-            std::fill(map.begin(), map.end(), 0u);
-            for (uint32_t u = 0; u < L.n_union; ++u) map[uni[u]] = u + 1;
-            std::vector<double> rows((size_t)(L.n_union + 1) * W, 0.0);
+        }
+        std::sort(uni.begin(), uni.end());
+        st.n_union = (uint32_t)uni.size();
+        for (uint32_t u = 0; u < st.n_union; ++u) map[uni[u]] = u + 1;
+        const size_t stride = (size_t)n_layers * W;
+        std::vector<double> rows((size_t)(st.n_union + 1) * stride, 0.0);
+        std::vector<ara::LayerTermsDev> lt(n_layers);
+        for (uint32_t l = 0; l < n_layers; ++l) {
+            const uint32_t E = st.n_cols[l];
             for (uint32_t c = 0; c < E; ++c) {
                 const uint32_t j = elt_index[elt_offsets[l] + c];
-                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
-                    rows[(size_t)map[ctx->rec_ids[r]] * W + c] = ctx->rec_losses[r];  // bit copy
-                L.terms.rate[c] = ctx->fin[j].rate;
-                L.terms.ret[c] = ctx->fin[j].retention;
-                L.terms.lim[c] = ctx->fin[j].limit;
+                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)  // bit copy
+                    rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W + c] =
+                        ctx->rec_losses[r];
+                lt[l].rate[c] = ctx->fin[j].rate;
+                lt[l].ret[c] = ctx->fin[j].retention;
+                lt[l].lim[c] = ctx->fin[j].limit;
             }
             for (uint32_t c = E; c < ara::kMaxCols; ++c) {  // neutral padding columns
-                L.terms.rate[c] = 1.0;
-                L.terms.ret[c] = 0.0;
-                L.terms.lim[c] = INFINITY;
+                lt[l].rate[c] = 1.0;
+                lt[l].ret[c] = 0.0;
+                lt[l].lim[c] = INFINITY;
             }
-            L.terms.occ_ret = terms[l].occ_retention;
-            L.terms.occ_lim = terms[l].occ_limit;
-            L.terms.agg_ret = terms[l].agg_retention;
-            L.terms.agg_lim = terms[l].agg_limit;
-            const size_t map_bytes = ((size_t)C + 1) * 4, row_bytes = rows.size() * 8;
-            cudaError_t e = cudaMalloc(&L.d_map, map_bytes);
-            if (e == cudaSuccess) e = cudaMalloc(&L.d_rows, row_bytes);
-            if (e == cudaSuccess)
-                e = cudaMemcpy(L.d_map, map.data(), map_bytes, cudaMemcpyHostToDevice);
-            if (e == cudaSuccess)
-                e = cudaMemcpy(L.d_rows, rows.data(), row_bytes, cudaMemcpyHostToDevice);
-            ctx->layers.push_back(L);
-            if (e != cudaSuccess) {
-                free_layers(ctx);
-                return cuda_fail(ctx, e, "device ELT store");
-            }
-            ctx->store_bytes += map_bytes + row_bytes;
+            lt[l].occ_ret = terms[l].occ_retention;
+            lt[l].occ_lim = terms[l].occ_limit;
+            lt[l].agg_ret = terms[l].agg_retention;
+            lt[l].agg_lim = terms[l].agg_limit;
         }
+        const size_t map_bytes = ((size_t)C + 1) * 4, row_bytes = rows.size() * 8,
+                     term_bytes = lt.size() * sizeof(ara::LayerTermsDev);
+        cudaError_t e = cudaMalloc(&st.d_map, map_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&st.d_rows, row_bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&st.d_terms, term_bytes);
+        if (e == cudaSuccess) e = cudaMemcpy(st.d_map, map.data(), map_bytes, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(st.d_rows, rows.data(), row_bytes, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(st.d_terms, lt.data(), term_bytes, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            free_layers(ctx);
+            return cuda_fail(ctx, e, "device ELT store");
+        }
+        ctx->store_bytes = map_bytes + row_bytes + term_bytes;
         ctx->have_layers = true;
         return ARA_OK;
     });
@@ -465,7 +472,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
         ara_status s = check_device_error(ctx);
         if (s != ARA_OK) return s;
 
-        const size_t n_layers = ctx->layers.size();
+        const size_t n_layers = ctx->store.n_layers;
         // device YLT staging
         if (ctx->ylt_stage_cap < n_layers * n_trials) {
             cudaFree(ctx->d_ylt_stage);
@@ -577,9 +584,8 @@ ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
     if (!ctx || !out) return ARA_ERR_ARG;
     out->catalogue_size = ctx->C;
     out->n_elts = ctx->n_elts;
-    out->n_layers = ctx->have_layers ? (uint32_t)ctx->layers.size() : 0;
-    out->max_row_width = 0;
-    for (auto &L : ctx->layers) out->max_row_width = std::max(out->max_row_width, L.width);
+    out->n_layers = ctx->have_layers ? ctx->store.n_layers : 0;
+    out->max_row_width = ctx->have_layers ? ctx->store.width : 0;
     out->store_bytes = ctx->store_bytes;
     out->kernel_launches = ctx->launches;
     out->device = ctx->device;
@@ -592,9 +598,9 @@ ara_status ara_layer_store_shape(const ara_ctx *ctx, uint32_t layer, uint32_t *n
 {
     if (!ctx) return ARA_ERR_ARG;
     if (!ctx->have_layers) return ARA_ERR_STATE;
-    if (layer >= ctx->layers.size()) return ARA_ERR_ARG;
-    if (n_union) *n_union = ctx->layers[layer].n_union;
-    if (row_width) *row_width = ctx->layers[layer].width;
+    if (layer >= ctx->store.n_layers) return ARA_ERR_ARG;
+    if (n_union) *n_union = ctx->store.n_union;
+    if (row_width) *row_width = ctx->store.width;
     return ARA_OK;
 }
 
@@ -602,14 +608,16 @@ ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, doubl
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "no layers");
-        if (layer >= ctx->layers.size()) return fail(ctx, ARA_ERR_ARG, "layer %u out of range", layer);
-        const ara::DeviceLayer &L = ctx->layers[layer];
+        const ara::DeviceStore &st = ctx->store;
+        if (layer >= st.n_layers) return fail(ctx, ARA_ERR_ARG, "layer %u out of range", layer);
         ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         if (h_map)
-            ARA_CUDA(ctx, cudaMemcpy(h_map, L.d_map, ((size_t)ctx->C + 1) * 4, cudaMemcpyDeviceToHost));
-        if (h_rows)
-            ARA_CUDA(ctx, cudaMemcpy(h_rows, L.d_rows, (size_t)(L.n_union + 1) * L.width * 8,
-                                     cudaMemcpyDeviceToHost));
+            ARA_CUDA(ctx, cudaMemcpy(h_map, st.d_map, ((size_t)ctx->C + 1) * 4, cudaMemcpyDeviceToHost));
+        if (h_rows)  // this layer's W columns of every union row
+            ARA_CUDA(ctx, cudaMemcpy2D(h_rows, (size_t)st.width * 8,
+                                       st.d_rows + (size_t)layer * st.width,
+                                       (size_t)st.n_layers * st.width * 8, (size_t)st.width * 8,
+                                       st.n_union + 1, cudaMemcpyDeviceToHost));
         return ARA_OK;
     });
 }

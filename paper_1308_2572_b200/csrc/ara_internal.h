@@ -14,11 +14,11 @@ namespace ara {
 
 constexpr int kMaxCols = ARA_MAX_ELTS_PER_LAYER;  // row width limit W (doubles)
 
-// Per-layer terms, passed by value as a kernel parameter (lives in the constant bank: every
-// lane reads the same address, the broadcast the paper got from constant memory, PAPER.md
-// L132).  Padded columns j >= E carry the neutral terms (rate 1, retention 0, limit +inf)
-// and zero losses, so F_j = +0 and lo + (+0) = lo exactly.
-struct ScanTerms {
+// Per-layer terms in device memory, one record per layer; every lane copies its own columns'
+// financial terms and its layer's occurrence / aggregate terms into registers at kernel start.
+// Padded columns j >= E carry the neutral terms (rate 1, retention 0, limit +inf) and zero
+// losses, so F_j = +0 and lo + (+0) = lo exactly (reading R12).
+struct LayerTermsDev {
     double rate[kMaxCols];
     double ret[kMaxCols];
     double lim[kMaxCols];
@@ -55,29 +55,33 @@ inline ScanShape scan_shape_for_width(uint32_t W, int override_g)
     return {4, (int)(W / 16)};
 }
 
-// Device ELT store of one layer: event-major rows.
-struct DeviceLayer {
-    uint32_t n_union = 0;   // U: distinct events over the layer's ELTs
-    uint32_t n_cols = 0;    // E: ELTs of the layer
-    uint32_t width = 0;     // W = row_width_for(E) doubles (whole 32-byte chunks)
-    int group_override = 0; // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
-    int min_blocks = 0;     // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
+// Device ELT store of all layers: one catalogue map shared by the
+// layers and event-major rows that hold every layer's columns back to back, so one id read and
+// one map lookup per event serve all layers (F1, the layer-fused portfolio pass).
+struct DeviceStore {
+    uint32_t n_layers = 0;
+    uint32_t n_union = 0;        // U: distinct events over all layers' ELTs
+    uint32_t width = 0;          // W = row_width_for(max E) doubles per layer
+    std::vector<uint32_t> n_cols;  // E of each layer
+    int group_override = 0;      // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
+    int min_blocks = 0;          // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
-    double *d_rows = nullptr;    // [(U+1) * W], row 0 zero
-    ScanTerms terms{};
+    double *d_rows = nullptr;    // [(U+1) * n_layers * W], row 0 zero
+    LayerTermsDev *d_terms = nullptr;  // [n_layers]
 };
 
 struct ScanLaunch {
     const uint64_t *offsets;  // [n+1], device
     const uint32_t *ids;      // device, indexed by offsets[t] - offsets[0]
-    double *ylt;              // [n], device
+    double *ylt;              // [n_layers][ld], device
+    uint64_t ylt_ld;          // YLT row stride (elements)
     uint64_t n_trials;
     uint32_t catalogue_size;
     uint32_t *err;            // device error word (bit 0: id out of range)
 };
 
 // scan.cu
-cudaError_t launch_scan(const DeviceLayer &L, const ScanLaunch &s, int sm_count,
+cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
                             uint32_t catalogue_size, uint32_t *err, int sm_count,

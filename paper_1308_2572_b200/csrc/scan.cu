@@ -124,25 +124,36 @@ __device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&r
     Cprev = Cd;
 }
 
-template <int CH, int W>
-__device__ __forceinline__ void gather(const double *__restrict__ my_rows, uint32_t idx,
-                                       Row4 (&r)[CH])
+template <int CH>
+__device__ __forceinline__ void gather(const double *__restrict__ my_rows, uint32_t stride,
+                                       uint32_t idx, Row4 (&r)[CH])
 {
+    const double *p = my_rows + (size_t)idx * stride;
 #pragma unroll
-    for (int i = 0; i < CH; ++i) load_row_chunk(my_rows + (size_t)idx * W + 4 * i, r[i]);
+    for (int i = 0; i < CH; ++i) load_row_chunk(p + 4 * i, r[i]);
 }
 
 template <int G, int CH, int MINB>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                const double *__restrict__ rows, const __grid_constant__ ScanTerms T)
+                const double *__restrict__ rows, const LayerTermsDev *__restrict__ terms,
+                uint32_t n_layers)
 {
-    constexpr int W = 4 * G * CH;  // row width (doubles)
+    constexpr int W = 4 * G * CH;  // row width per layer (doubles)
     constexpr int NCOL = 4 * CH;   // columns per lane
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;   // this lane's position in its group
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - c));
 
+    // Group g works on (trial g / L + i * stride, layer g % L): the launch makes the number of
+    // groups a multiple of L, so a lane's layer is fixed and consecutive groups share a trial
+    // (its id and map requests coalesce).
+    const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
+    const uint32_t layer = (uint32_t)(g % n_layers);
+    const uint64_t t_stride = groups / n_layers;
+
+    const LayerTermsDev &T = terms[layer];
     double rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
@@ -152,14 +163,14 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     }
     const double occ_ret = T.occ_ret, occ_lim = T.occ_lim;
     const double agg_ret = T.agg_ret, agg_lim = T.agg_lim;
-    const double *__restrict__ my_rows = rows + NCOL * c;
+    const uint32_t row_stride = n_layers * W;  // doubles per union row
+    const double *__restrict__ my_rows = rows + (size_t)layer * W + NCOL * c;
     const uint32_t C = s.catalogue_size;
+    double *const ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
 
-    const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
     const uint64_t base = s.offsets[0];
     bool bad = false;
-    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; t < s.n_trials;
-         t += groups) {
+    for (uint64_t t = g / n_layers; t < s.n_trials; t += t_stride) {
         const uint64_t beg = s.offsets[t] - base;
         const uint64_t k = s.offsets[t + 1] - base - beg;
         const uint32_t *ev = s.ids + beg;
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Row4 r[CH];
-            gather<CH, W>(my_rows, map_index(map, load_id(ev), C, bad), r);
+            gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
             event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr);
             ++ev;
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             uint32_t idx0 = map_index(map, id_c[0], C, bad);
             uint32_t idx1 = map_index(map, id_c[1], C, bad);
             Row4 ra[CH];
-            gather<CH, W>(my_rows, idx0, ra);
+            gather<CH>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
             for (uint64_t i = 0; i < n_chunks; ++i) {
                 const bool more = i + 1 < n_chunks;
@@ -197,11 +208,11 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     const bool ok2 = j + 2 < 8 || more;
                     uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
                     Row4 rb[CH];
-                    gather<CH, W>(my_rows, pin(idx1, S), rb);
+                    gather<CH>(my_rows, row_stride, pin(idx1, S), rb);
                     event_step<G, CH>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr);
                     uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
-                    gather<CH, W>(my_rows, pin(idx2, S), ra);  // event j+2 (zero row past end)
+                    gather<CH>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
                     event_step<G, CH>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr);
                     idx1 = idx3;
@@ -215,12 +226,12 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // tail: remaining events one by one
         while (ev < ev_end) {
             Row4 r[CH];
-            gather<CH, W>(my_rows, map_index(map, load_id(ev), C, bad), r);
+            gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
             event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr);
             ++ev;
         }
-        if (c == G - 1) s.ylt[t] = lr;  // A8
+        if (c == G - 1) ylt_row[t] = lr;  // A8
     }
     if (bad) atomicOr(s.err, kErrRange);
 }
@@ -246,7 +257,8 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
 }
 
 template <int G, int CH, int MINB = 1>
-cudaError_t launch_gc(const DeviceLayer &L, const ScanLaunch &s, int sm_count, cudaStream_t stream)
+cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                      cudaStream_t stream)
 {
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
@@ -255,46 +267,57 @@ cudaError_t launch_gc(const DeviceLayer &L, const ScanLaunch &s, int sm_count, c
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
-    // Balanced single wave: every group gets ceil(n / groups) or one fewer trials, and the
-    // grid is a multiple of the SM count so every SM holds the same number of groups.
+    // Balanced single wave over (trial, layer) groups: every trial slot gets ceil(n / slots)
+    // or one fewer trials; the number of groups is a multiple of L (a lane keeps its layer) and,
+    // where possible, the grid is a multiple of the SM count.
+    const uint64_t L = st.n_layers;
     const uint64_t per_block = kScanThreads / G;
-    const uint64_t groups_max = (uint64_t)sm_count * occ * per_block;
-    const uint64_t rounds = (s.n_trials + groups_max - 1) / groups_max;
-    const uint64_t groups = (s.n_trials + rounds - 1) / rounds;
-    uint64_t blocks = (groups + per_block - 1) / per_block;
-    if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
-    if (blocks > (uint64_t)sm_count * occ) blocks = (uint64_t)sm_count * occ;
-    scan_kernel<G, CH, MINB><<<(unsigned)blocks, kScanThreads, 0, stream>>>(s, L.d_map, L.d_rows, L.terms);
+    uint64_t m = L;  // blocks must be a multiple of m = L / gcd(L, per_block)
+    for (uint64_t a = L, b = per_block; b;) { const uint64_t r = a % b; a = b; b = r; m = L / a; }
+    const uint64_t max_blocks = (uint64_t)sm_count * occ / m * m;
+    if (max_blocks == 0) return cudaErrorInvalidConfiguration;
+    const uint64_t slots_max = max_blocks * per_block / L;
+    const uint64_t rounds = (s.n_trials + slots_max - 1) / slots_max;
+    const uint64_t slots = (s.n_trials + rounds - 1) / rounds;
+    uint64_t blocks = (slots * L + per_block - 1) / per_block;
+    blocks = (blocks + m - 1) / m * m;
+    uint64_t lcm = m;
+    while (lcm % (uint64_t)sm_count) lcm += m;
+    if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
+        blocks = (blocks + lcm - 1) / lcm * lcm;
+    if (blocks > max_blocks) blocks = max_blocks;
+    scan_kernel<G, CH, MINB><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
+        s, st.d_map, st.d_rows, st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_scan(const DeviceLayer &L, const ScanLaunch &s, int sm_count,
+cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches)
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
-    const ScanShape sh = scan_shape_for_width(L.width, L.group_override);
+    const ScanShape sh = scan_shape_for_width(st.width, st.group_override);
     switch (sh.G * 16 + sh.CH) {
-        case 1 * 16 + 1: return launch_gc<1, 1>(L, s, sm_count, stream);
-        case 2 * 16 + 1: return launch_gc<2, 1>(L, s, sm_count, stream);
+        case 1 * 16 + 1: return launch_gc<1, 1>(st, s, sm_count, stream);
+        case 2 * 16 + 1: return launch_gc<2, 1>(st, s, sm_count, stream);
         case 4 * 16 + 1:  // W = 16 with G = 4 (tuning)
-            switch (L.min_blocks) {
-                case 5: return launch_gc<4, 1, 5>(L, s, sm_count, stream);
-                case 6: return launch_gc<4, 1, 6>(L, s, sm_count, stream);
-                default: return launch_gc<4, 1>(L, s, sm_count, stream);
+            switch (st.min_blocks) {
+                case 5: return launch_gc<4, 1, 5>(st, s, sm_count, stream);
+                case 6: return launch_gc<4, 1, 6>(st, s, sm_count, stream);
+                default: return launch_gc<4, 1>(st, s, sm_count, stream);
             }
-        case 4 * 16 + 2: return launch_gc<4, 2>(L, s, sm_count, stream);
-        case 4 * 16 + 3: return launch_gc<4, 3>(L, s, sm_count, stream);
-        case 4 * 16 + 4: return launch_gc<4, 4>(L, s, sm_count, stream);
+        case 4 * 16 + 2: return launch_gc<4, 2>(st, s, sm_count, stream);
+        case 4 * 16 + 3: return launch_gc<4, 3>(st, s, sm_count, stream);
+        case 4 * 16 + 4: return launch_gc<4, 4>(st, s, sm_count, stream);
         case 2 * 16 + 2:  // W = 16 (default)
-            switch (L.min_blocks) {
-                case 4: return launch_gc<2, 2, 4>(L, s, sm_count, stream);
-                case 5: return launch_gc<2, 2, 5>(L, s, sm_count, stream);
-                default: return launch_gc<2, 2>(L, s, sm_count, stream);
+            switch (st.min_blocks) {
+                case 4: return launch_gc<2, 2, 4>(st, s, sm_count, stream);
+                case 5: return launch_gc<2, 2, 5>(st, s, sm_count, stream);
+                default: return launch_gc<2, 2>(st, s, sm_count, stream);
             }
-        case 1 * 16 + 4: return launch_gc<1, 4>(L, s, sm_count, stream);  // W = 16 with G = 1
+        case 1 * 16 + 4: return launch_gc<1, 4>(st, s, sm_count, stream);  // W = 16, G = 1
         default: --*launches; return cudaErrorInvalidValue;
     }
 }

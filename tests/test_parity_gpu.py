@@ -335,3 +335,26 @@ def test_headline_size_sampled(stream):
     sel = np.concatenate([sel, np.array([0, ds.n_trials - 1], np.uint64)])
     want = oracle.run_analysis(ds, selection=sel, n_threads=8)
     assert_bit_identical(got[:, sel.astype(np.int64)], want)
+
+
+def test_layers_of_different_widths(stream):
+    """Layers of 3, 16, 7 and 1 ELTs in one fused pass (all padded to the widest row, W = 16);
+    ELTs listed in non-monotone order and shared between layers."""
+    spec = datagen.PRESETS["tiny"].replace(n_elts=20, elts_per_layer=2, n_trials=900, k_min=0,
+                                           k_max=50, seed=11)
+    ds = datagen.generate(spec)
+    members = [[5, 0, 19], list(range(16)), [7, 3, 11, 2, 18, 0, 9], [12]]
+    ds.elt_offsets = np.cumsum([0] + [len(m) for m in members]).astype(np.uint32)
+    ds.elt_index = np.concatenate([np.array(m, np.uint32) for m in members])
+    ds.layer_terms = np.array([[10.0, 5e4, 1e4, 2e5], [0.0, math.inf, 0.0, math.inf],
+                               [500.0, 1e5, 5e5, 1e6], [0.0, 1e3, 0.0, 5e3]])
+    want = oracle.run_analysis(ds)
+    got = gpu_ylt(types_ns(ds), stream)
+    assert_bit_identical(got, want)
+
+
+def types_ns(ds):
+    import types
+    return types.SimpleNamespace(**{k: getattr(ds, k) for k in (
+        "catalogue_size", "rec_offsets", "rec_event_ids", "rec_losses", "fin", "layer_terms",
+        "elt_offsets", "elt_index", "trial_offsets", "events")}, n_layers=ds.elt_offsets.shape[0] - 1)

@@ -36,7 +36,8 @@ def main():
     d_ids = torch.from_numpy(ds.events.view(np.int32)).to(dev).view(torch.uint32)
     E = spec.elts_per_layer
     n, n_ev = ds.n_trials, int(ds.trial_offsets[-1])
-    bytes_alg = (n_ev * (4 + 8 * E) + 8 * n + 8 * (n + 1)) * ds.n_layers
+    L = ds.n_layers
+    bytes_alg = n_ev * (4 + 8 * E * L) + 8 * n * L + 8 * (n + 1)
     ref = None
     for v in args.variants.split(","):
         g, mb = v.split(":")
