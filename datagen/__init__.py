@@ -109,6 +109,15 @@ PRESETS = {
                          layer_stride=8, n_trials=1_000_000,
                          occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4772, agg_lim_m=0.0461),
 }
+# configs[4] scaling sweep (F2): events per trial 500-2000 and variable 800-1500,
+# ELTs per layer 4-64, trials up to 8M.  Same generator, multipliers as the headline.
+for _e in (4, 8, 16, 32, 64):
+    PRESETS[f"sweep-e{_e}"] = PRESETS["headline"].replace(
+        name=f"sweep-e{_e}", n_elts=_e, elts_per_layer=_e)
+for _k in (500, 2000):
+    PRESETS[f"sweep-k{_k}"] = PRESETS["headline"].replace(name=f"sweep-k{_k}", k_min=_k, k_max=_k)
+PRESETS["sweep-ragged"] = PRESETS["headline"].replace(name="sweep-ragged", k_min=800, k_max=1500)
+PRESETS["sweep-n8m"] = PRESETS["headline"].replace(name="sweep-n8m", n_trials=8_000_000)
 
 
 @dataclasses.dataclass

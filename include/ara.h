@@ -81,6 +81,9 @@ typedef struct {
 #define ARA_RUN_VALIDATE 2u /* check offsets and event ids on the device BEFORE the scan
                                (one extra YET read); implies ARA_RUN_SYNC; on error nothing
                                is written to the YLT                                        */
+#define ARA_RUN_BALANCE 4u  /* hand trials to thread groups dynamically (one atomic ticket
+                               per trial and layer): use for variable-length trials (PAPER.md
+                               L43: 800-1500 events); results are identical either way      */
 
 /* Human-readable name of a status code (static storage). */
 const char *ara_status_string(ara_status s);
@@ -146,7 +149,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
  *   d_event_ids[]             device, u32 catalogue ids in [1, C]
  *   d_ylt                     device, fp64, YLT[l][t] at d_ylt[l * ylt_ld + t]
  *   ylt_ld                    row stride of the YLT in elements (0 means n_trials)
- *   flags                     ARA_RUN_SYNC | ARA_RUN_VALIDATE
+ *   flags                     ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE
  * Without ARA_RUN_SYNC the call only enqueues work on the context stream and returns ARA_OK;
  * an event id outside [1, C] then reads the zero row (never out of bounds) and sets a device
  * error flag that the next ara_synchronize() (or synchronous call) reports as ARA_ERR_RANGE.

@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "ARA_OK", 1: "ARA_ERR_ARG", 2: "ARA_ERR_RANGE", 3: "ARA_ERR_V
                 8: "ARA_ERR_UNSUPPORTED"}
 ARA_RUN_SYNC = 1
 ARA_RUN_VALIDATE = 2
+ARA_RUN_BALANCE = 4
 ARA_MAX_ELTS_PER_LAYER = 64
 ARA_MAX_P = 32
 

@@ -9,6 +9,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <new>
@@ -38,6 +39,8 @@ struct ara_ctx {
     uint64_t store_bytes = 0;
 
     uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
+    unsigned long long *d_ticket = nullptr;  // dynamic scheduling: ticket + done counters
+    int sched = 0;              // 0 auto, 1 static, 2 dynamic (env ARA_SCAN_SCHED)
     uint32_t *h_err = nullptr;  // pinned mirror
     uint64_t launches = 0;
     ara::MetricsScratch metrics;
@@ -154,9 +157,17 @@ ara_status check_device_error(ara_ctx *ctx)
 // One scan launch covers every layer (layer-fused pass: one id read and one map lookup per
 // event serve all layers).
 ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const uint32_t *d_ids,
-                         double *d_ylt, uint64_t ld)
+                         double *d_ylt, uint64_t ld, uint32_t flags)
 {
-    ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err};
+    // Dynamic ticket scheduling (one atomic per trial and layer) balances variable-length
+    // trials; it is the default for a single layer.  With several layers the static
+    // assignment keeps the groups of one trial side by side (shared id and map requests)
+    // unless ARA_RUN_BALANCE asks for dynamic tickets.  Results are identical either way.
+    const bool dyn = ctx->sched == 2 ||
+                     (ctx->sched == 0 && ((flags & ARA_RUN_BALANCE) || ctx->store.n_layers == 1));
+    ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
+                      dyn ? ctx->d_ticket : nullptr,
+                      dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr};
     cudaError_t e = ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
@@ -198,6 +209,10 @@ ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
                                            cuda_device);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 4);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_ticket, 16);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_ticket, 0, 16);
+    if (const char *sc = getenv("ARA_SCAN_SCHED"))
+        ctx->sched = strcmp(sc, "static") == 0 ? 1 : strcmp(sc, "dynamic") == 0 ? 2 : 0;
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, 4);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -228,6 +243,7 @@ void ara_destroy(ara_ctx *ctx)
     cudaStreamSynchronize(ctx->stream);
     free_layers(ctx);
     cudaFree(ctx->d_err);
+    cudaFree(ctx->d_ticket);
     cudaFreeHost(ctx->h_err);
     cudaFree(ctx->metrics.d_buf);
     for (int i = 0; i < 2; ++i) {
@@ -418,7 +434,7 @@ ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offs
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
-        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE))
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
         if (n_trials == 0) return ARA_OK;
         if (!d_trial_offsets || !d_event_ids || !d_ylt)
@@ -435,7 +451,7 @@ ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offs
             s = check_device_error(ctx);
             if (s != ARA_OK) return s;
         }
-        ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, d_ylt, ld);
+        ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, d_ylt, ld, flags);
         if (s != ARA_OK) return s;
         if (flags & (ARA_RUN_SYNC | ARA_RUN_VALIDATE)) return check_device_error(ctx);
         return ARA_OK;
@@ -456,7 +472,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
-        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE))
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
         if (n_trials == 0) return ARA_OK;
         if (!h_trial_offsets || !h_ylt) return fail(ctx, ARA_ERR_ARG, "host pointer is NULL");
@@ -524,7 +540,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
             ARA_CUDA(ctx, cudaEventRecord(ctx->ev_copy[buf], ctx->copy_stream));
             ARA_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copy[buf], 0));
             s = launch_layers(ctx, t1 - t0, ctx->d_off_stage[buf], ctx->d_ids_stage[buf],
-                              ctx->d_ylt_stage + t0, n_trials);
+                              ctx->d_ylt_stage + t0, n_trials, flags);
             if (s != ARA_OK) return s;
             ARA_CUDA(ctx, cudaEventRecord(ctx->ev_done[buf], ctx->stream));
             used[buf] = true;

@@ -78,6 +78,8 @@ struct ScanLaunch {
     uint64_t n_trials;
     uint32_t catalogue_size;
     uint32_t *err;            // device error word (bit 0: id out of range)
+    unsigned long long *counter;  // dynamic ticket counter (NULL: static assignment)
+    unsigned int *done;           // finished-block counter (resets `counter`)
 };
 
 // scan.cu

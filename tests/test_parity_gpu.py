@@ -358,3 +358,21 @@ def types_ns(ds):
     return types.SimpleNamespace(**{k: getattr(ds, k) for k in (
         "catalogue_size", "rec_offsets", "rec_event_ids", "rec_losses", "fin", "layer_terms",
         "elt_offsets", "elt_index", "trial_offsets", "events")}, n_layers=ds.elt_offsets.shape[0] - 1)
+
+
+@pytest.mark.parametrize("preset,k", [("tiny", (0, 60)), ("portfolio", (50, 300))])
+def test_dynamic_balance_scheduling(stream, preset, k):
+    """ARA_RUN_BALANCE hands (trial, layer) tickets out dynamically: same YLT bit for bit, every
+    entry written (the YLT starts as NaN), and the ticket counter resets itself between
+    back-to-back launches (a stale counter would skip trials)."""
+    spec = datagen.PRESETS[preset].replace(n_trials=1500, k_min=k[0], k_max=k[1], seed=5)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds, n_threads=8)
+    ctx = make_ctx(ds, stream)
+    for _ in range(3):
+        got = gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_BALANCE)
+        assert_bit_identical(got, want)
+    # interleave with static launches on the same context
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_BALANCE), want)
+    ctx.close()

@@ -23,7 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="headline")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--variants", default="4:0,4:3,4:4,2:0,2:3,1:0")
+    ap.add_argument("--variants", default="2:0,4:0,1:0")
+    ap.add_argument("--flags", type=int, default=0, help="ara_run flags (4 = ARA_RUN_BALANCE)")
+    ap.add_argument("--sched", default="", help="ARA_SCAN_SCHED: static | dynamic")
     args = ap.parse_args()
     import torch
 
@@ -43,19 +45,20 @@ def main():
         g, mb = v.split(":")
         os.environ["ARA_SCAN_GROUP"] = g
         os.environ["ARA_SCAN_MINB"] = mb
+        os.environ["ARA_SCAN_SCHED"] = args.sched
         ctx = ara.Context(0, stream)
         ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses,
                           ds.fin)
         ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
         ylt = torch.empty((ds.n_layers, n), dtype=torch.float64, device=dev)
         for _ in range(3):
-            ctx.ara_run(d_off, d_ids, ylt)
+            ctx.ara_run(d_off, d_ids, ylt, flags=args.flags)
         ctx.ara_synchronize()
         ts = []
         for _ in range(args.reps):
             a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            ctx.ara_run(d_off, d_ids, ylt)
+            ctx.ara_run(d_off, d_ids, ylt, flags=args.flags)
             b.record(stream)
             b.synchronize()
             ts.append(a.elapsed_time(b))
@@ -64,7 +67,8 @@ def main():
         same = True if ref is None else bool(np.array_equal(out, ref))
         ref = out if ref is None else ref
         ms = float(np.median(ts))
-        print(json.dumps({"variant": v, "config": args.config, "ms_median": ms,
+        print(json.dumps({"variant": v, "sched": args.sched or f"flags={args.flags}",
+                          "config": args.config, "ms_median": ms,
                           "ms_min": float(min(ts)), "GBps_alg": bytes_alg / ms / 1e6,
                           "trial_events_per_s": n_ev * ds.n_layers / ms * 1e3,
                           "same_as_first": same}), flush=True)
