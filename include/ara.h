@@ -159,6 +159,35 @@ ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offs
                    const uint32_t *d_event_ids, double *d_ylt, uint64_t ylt_ld, uint32_t flags);
 
 /*
+ * ara_run_outputs -- ara_run with the optional per-trial and per-event outputs of the same pass
+ * (YLT consumers; "financial functions or filters are then
+ * applied on the aggregate loss values"):
+ *   ylt, ylt_ld               as ara_run (required)
+ *   max_occ, max_occ_ld       optional [n_layers][ld] device fp64: per (layer, trial) the largest
+ *                             occurrence loss lo_d after line 16 (0 for an empty trial); its
+ *                             distribution is the occurrence exceedance (OEP) curve, e.g.
+ *                             ara_metrics on a max_occ row gives OEP PML / TVaR
+ *   event_inc, event_inc_ld   optional [n_layers][ld] device fp64: the incremental aggregate
+ *                             loss of lines 24-26 of every event, stored at the event's YET
+ *                             position offsets[t] - offsets[0] + d (ld >= the YET's event count;
+ *                             0 means exactly that count); a trial's entries sum to lr (line 28)
+ *                             and allocate the trial loss to its events
+ * A leading dimension of 0 means the minimum.  Requesting event_inc costs one synchronous read of
+ * offsets[0] and offsets[n] (to check ld).  Errors: as ara_run.
+ */
+typedef struct {
+    double *ylt;
+    uint64_t ylt_ld;
+    double *max_occ;
+    uint64_t max_occ_ld;
+    double *event_inc;
+    uint64_t event_inc_ld;
+} ara_outputs;
+
+ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
+                           const uint32_t *d_event_ids, const ara_outputs *out, uint32_t flags);
+
+/*
  * ara_run_host -- ara_run with HOST buffers (end-to-end path): h_trial_offsets[n+1] and
  * h_event_ids as in ara_run but in host memory (page-locked memory gives full PCIe bandwidth),
  * h_ylt[l * ylt_ld + t] in host memory.  The YET is streamed to the device in chunks on the

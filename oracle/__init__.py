@@ -53,6 +53,9 @@ def lib() -> ctypes.CDLL:
         L.oracle_run_analysis.argtypes = [u32, u32, p, p, p, p, u32, p, p, p, u64, p, p,
                                           u64, p, p, ctypes.c_int]
         L.oracle_run_analysis.restype = ctypes.c_int
+        L.oracle_run_analysis_ex.argtypes = [u32, u32, p, p, p, p, u32, p, p, p, u64, p, p,
+                                             u64, p, p, p, p, ctypes.c_int]
+        L.oracle_run_analysis_ex.restype = ctypes.c_int
         L.oracle_metrics.argtypes = [p, u64, u32, p, p, p]
         L.oracle_metrics.restype = ctypes.c_int
         _lib = L
@@ -96,7 +99,7 @@ def build_dat(catalogue_size: int, event_ids, losses) -> np.ndarray:
 
 
 def run_analysis(ds, selection: Optional[np.ndarray] = None, n_threads: int = 1,
-                 trial_offsets=None, events=None) -> np.ndarray:
+                 trial_offsets=None, events=None, outputs: bool = False):
     """YLT[n_layers][n] of Algorithm 1.
 
     ``ds`` carries numpy arrays: catalogue_size, rec_offsets, rec_event_ids, rec_losses,
@@ -118,21 +121,25 @@ def run_analysis(ds, selection: Optional[np.ndarray] = None, n_threads: int = 1,
     sel = None if selection is None else c(selection, np.uint64)
     n_out = n_trials if sel is None else sel.shape[0]
     ylt = np.zeros((n_layers, n_out), dtype=np.float64)
+    n_ev = int(to[-1] - to[0]) if to.size else 0
+    mo = np.zeros((n_layers, n_out)) if outputs else None
+    inc = np.zeros((n_layers, max(n_ev, 1))) if outputs else None
     if n_layers == 0 or n_out == 0:
-        return ylt
-    st = lib().oracle_run_analysis(
+        return (ylt, mo, inc[:, :n_ev]) if outputs else ylt
+    st = lib().oracle_run_analysis_ex(
         int(ds.catalogue_size), rec_off.shape[0] - 1, _ptr(rec_off), _ptr(rec_ids),
         _ptr(rec_ls), _ptr(fin), n_layers, _ptr(lt), _ptr(eo),
         _ptr(ei) if ei.size else None, n_trials, _ptr(to),
         _ptr(ev) if ev.size else None, 0 if sel is None else sel.shape[0],
-        None if sel is None else _ptr(sel), _ptr(ylt), int(n_threads))
+        None if sel is None else _ptr(sel), _ptr(ylt), _ptr(mo) if outputs else None,
+        _ptr(inc) if outputs else None, int(n_threads))
     if st == -1:
         raise MemoryError("oracle: out of memory")
     if st == -3:
         raise ValueError("oracle: trial event id outside [1, catalogue_size]")
     if st < -1:
         raise ValueError(f"oracle: ELT record {-st - 2} has an invalid event id")
-    return ylt
+    return (ylt, mo, inc[:, :n_ev]) if outputs else ylt
 
 
 def metrics(ylt_row, p: Sequence[float]):

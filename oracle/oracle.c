@@ -25,6 +25,10 @@
  *   R6 an absent limit is +infinity.
  *   R7 sums are left-to-right: over ELTs in the layer's listed order (lines 11-13), over
  *      events in trial order (line 19, line 28).
+ *   F4 outputs: max_occ[l][t] = max over the trial's events of lo_d after line 16 (the
+ *      per-trial maximum occurrence loss, whose distribution is the OEP curve; 0 for an empty
+ *      trial); inc[l][pos] = the per-event incremental aggregate loss of lines 24-26 at the
+ *      event's position in the YET (the back-allocation of lr to events).
  *   R11 PML(p) = nearest-rank v[ceil(p*n) - 1] of the ascending YLT row; TVaR(p) = mean of
  *      all v >= PML(p).  The paper only names the metrics.
  */
@@ -128,7 +132,10 @@ static void o_work_free(o_work *w)
     memset(w, 0, sizeof(*w));
 }
 
-static double o_run_trial(const o_layer *a, const uint32_t *events, uint64_t k, o_work *w)
+/* Returns lr; *max_occ = max_d lo_d after line 16 (0 for an empty trial); the per-event
+ * increments of lines 24-26 are left in w->inc[0..k). */
+static double o_run_trial(const o_layer *a, const uint32_t *events, uint64_t k, o_work *w,
+                          double *max_occ)
 {
     for (uint64_t d = 0; d < k; ++d) w->lo[d] = 0.0;               /* R4 */
     for (uint32_t c = 0; c < a->n_elts; ++c) {                      /* line 4 */
@@ -141,6 +148,9 @@ static double o_run_trial(const o_layer *a, const uint32_t *events, uint64_t k, 
     }
     for (uint64_t d = 0; d < k; ++d)                                /* lines 15-17 */
         w->lo[d] = oracle_apply_occurrence_terms(w->lo[d], a->occ_retention, a->occ_limit);
+    double m = 0.0;                                                 /* F4: OEP basis */
+    for (uint64_t d = 0; d < k; ++d) m = (m < w->lo[d]) ? w->lo[d] : m;
+    *max_occ = m;
     oracle_apply_aggregate_terms(w->lo, k, a->agg_retention, a->agg_limit, w->cum,
                                  w->inc);                           /* lines 18-26 */
     double lr = 0.0;                                                /* R4 */
@@ -161,6 +171,9 @@ typedef struct {
     const uint64_t *selection;  /* NULL: trials [t0, t1); else selected trial indices */
     uint64_t t0, t1;            /* range of trials (or of selection entries) */
     double *ylt;                /* [n_layers][n_out] */
+    double *max_occ;            /* NULL or [n_layers][n_out] */
+    double *inc;                /* NULL or [n_layers][n_events] (positions of the whole YET) */
+    uint64_t n_events;
     uint64_t n_out;
     int status;
 } o_job;
@@ -175,8 +188,16 @@ static void *o_job_run(void *arg)
         const uint32_t *ev = j->events + (j->trial_offsets[t] - j->trial_offsets[0]);
         uint64_t k = j->trial_offsets[t + 1] - j->trial_offsets[t];
         if (o_work_reserve(&w, k)) { j->status = -1; break; }
-        for (uint32_t a = 0; a < j->n_layers; ++a)
-            j->ylt[(uint64_t)a * j->n_out + i] = o_run_trial(&j->layers[a], ev, k, &w);
+        for (uint32_t a = 0; a < j->n_layers; ++a) {
+            double m;
+            j->ylt[(uint64_t)a * j->n_out + i] = o_run_trial(&j->layers[a], ev, k, &w, &m);
+            if (j->max_occ) j->max_occ[(uint64_t)a * j->n_out + i] = m;
+            if (j->inc) {
+                double *dst = j->inc + (uint64_t)a * j->n_events +
+                              (j->trial_offsets[t] - j->trial_offsets[0]);
+                for (uint64_t d = 0; d < k; ++d) dst[d] = w.inc[d];
+            }
+        }
     }
     o_work_free(&w);
     return NULL;
@@ -194,13 +215,14 @@ static void *o_job_run(void *arg)
  * Returns 0; -1 out of memory; -(2+r) if record r has an invalid event id; -3 for a
  * trial event outside [1, C].
  */
-int oracle_run_analysis(uint32_t catalogue_size, uint32_t n_elts, const uint64_t *rec_offsets,
-                        const uint32_t *rec_event_ids, const double *rec_losses,
-                        const double *fin, uint32_t n_layers, const double *layer_terms,
-                        const uint32_t *elt_offsets, const uint32_t *elt_index,
-                        uint64_t n_trials, const uint64_t *trial_offsets,
-                        const uint32_t *events, uint64_t n_sel, const uint64_t *selection,
-                        double *ylt, int n_threads)
+int oracle_run_analysis_ex(uint32_t catalogue_size, uint32_t n_elts,
+                           const uint64_t *rec_offsets, const uint32_t *rec_event_ids,
+                           const double *rec_losses, const double *fin, uint32_t n_layers,
+                           const double *layer_terms, const uint32_t *elt_offsets,
+                           const uint32_t *elt_index, uint64_t n_trials,
+                           const uint64_t *trial_offsets, const uint32_t *events, uint64_t n_sel,
+                           const uint64_t *selection, double *ylt, double *max_occ,
+                           double *inc, int n_threads)
 {
     int status = 0;
     uint64_t n_ev = trial_offsets[n_trials] - trial_offsets[0];
@@ -255,6 +277,7 @@ int oracle_run_analysis(uint32_t catalogue_size, uint32_t n_elts, const uint64_t
         j->layers = layers; j->n_layers = n_layers;
         j->trial_offsets = trial_offsets; j->events = events; j->n_trials = n_trials;
         j->selection = selection; j->ylt = ylt; j->n_out = n_out;
+        j->max_occ = max_occ; j->inc = inc; j->n_events = n_ev;
         j->t0 = n_out * (uint64_t)i / (uint64_t)n_threads;
         j->t1 = n_out * (uint64_t)(i + 1) / (uint64_t)n_threads;
     }
@@ -268,6 +291,20 @@ done:
     if (dats) for (uint32_t j = 0; j < n_elts; ++j) free(dats[j]);
     free(dats); free(layers); free(dat_refs); free(terms3);
     return status;
+}
+
+int oracle_run_analysis(uint32_t catalogue_size, uint32_t n_elts, const uint64_t *rec_offsets,
+                        const uint32_t *rec_event_ids, const double *rec_losses,
+                        const double *fin, uint32_t n_layers, const double *layer_terms,
+                        const uint32_t *elt_offsets, const uint32_t *elt_index,
+                        uint64_t n_trials, const uint64_t *trial_offsets,
+                        const uint32_t *events, uint64_t n_sel, const uint64_t *selection,
+                        double *ylt, int n_threads)
+{
+    return oracle_run_analysis_ex(catalogue_size, n_elts, rec_offsets, rec_event_ids, rec_losses,
+                                  fin, n_layers, layer_terms, elt_offsets, elt_index, n_trials,
+                                  trial_offsets, events, n_sel, selection, ylt, NULL, NULL,
+                                  n_threads);
 }
 
 /* ------------------------------------------------------------------------- */

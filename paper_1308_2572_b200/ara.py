@@ -28,7 +28,8 @@ ARA_MAX_P = 32
 
 # Every symbol include/ara.h declares (tests check the library exports all of them).
 EXPORTS = ["ara_status_string", "ara_create", "ara_set_stream", "ara_destroy", "ara_last_error",
-           "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_host", "ara_synchronize",
+           "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
+           "ara_synchronize",
            "ara_metrics", "ara_metrics_host", "ara_get_info", "ara_layer_store_shape",
            "ara_export_store"]
 
@@ -52,6 +53,12 @@ class FinTerms(ctypes.Structure):
 class LayerTerms(ctypes.Structure):
     _fields_ = [("occ_retention", ctypes.c_double), ("occ_limit", ctypes.c_double),
                 ("agg_retention", ctypes.c_double), ("agg_limit", ctypes.c_double)]
+
+
+class Outputs(ctypes.Structure):
+    _fields_ = [("ylt", ctypes.c_void_p), ("ylt_ld", ctypes.c_uint64),
+                ("max_occ", ctypes.c_void_p), ("max_occ_ld", ctypes.c_uint64),
+                ("event_inc", ctypes.c_void_p), ("event_inc_ld", ctypes.c_uint64)]
 
 
 class Info(ctypes.Structure):
@@ -78,6 +85,7 @@ def _load() -> ctypes.CDLL:
         "ara_load_elts": ([p, u32, u32, p, p, p, p], i32),
         "ara_set_layers": ([p, u32, p, p, p], i32),
         "ara_run": ([p, u64, p, p, p, u64, u32], i32),
+        "ara_run_outputs": ([p, u64, p, p, ctypes.POINTER(Outputs), u32], i32),
         "ara_run_host": ([p, u64, p, p, p, u64, u32], i32),
         "ara_synchronize": ([p], i32),
         "ara_metrics": ([p, p, u64, u32, p, p, p], i32),
@@ -186,6 +194,18 @@ class Context:
         self._check(lib().ara_run(self._ptr, n, _dptr(d_trial_offsets, "torch.uint64"),
                                   _dptr(d_event_ids, "torch.uint32"),
                                   _dptr(d_ylt, "torch.float64"), ylt_ld, flags))
+
+    def ara_run_outputs(self, d_trial_offsets, d_event_ids, d_ylt, d_max_occ=None,
+                        d_event_inc=None, flags: int = 0, ylt_ld: int = 0, max_occ_ld: int = 0,
+                        event_inc_ld: int = 0):
+        o = Outputs(_dptr(d_ylt, "torch.float64"), ylt_ld,
+                    None if d_max_occ is None else _dptr(d_max_occ, "torch.float64"), max_occ_ld,
+                    None if d_event_inc is None else _dptr(d_event_inc, "torch.float64"),
+                    event_inc_ld)
+        self._check(lib().ara_run_outputs(self._ptr, d_trial_offsets.numel() - 1,
+                                          _dptr(d_trial_offsets, "torch.uint64"),
+                                          _dptr(d_event_ids, "torch.uint32"), ctypes.byref(o),
+                                          flags))
 
     def ara_run_host(self, h_trial_offsets, h_event_ids, h_ylt: np.ndarray, ylt_ld: int = 0,
                      flags: int = 0):

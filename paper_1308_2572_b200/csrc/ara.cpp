@@ -157,7 +157,8 @@ ara_status check_device_error(ara_ctx *ctx)
 // One scan launch covers every layer (layer-fused pass: one id read and one map lookup per
 // event serve all layers).
 ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const uint32_t *d_ids,
-                         double *d_ylt, uint64_t ld, uint32_t flags)
+                         double *d_ylt, uint64_t ld, uint32_t flags,
+                         const ara_outputs *extra = nullptr)
 {
     // Dynamic ticket scheduling (one atomic per trial and layer) balances variable-length
     // trials; it is the default for a single layer.  With several layers the static
@@ -167,7 +168,9 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                      (ctx->sched == 0 && ((flags & ARA_RUN_BALANCE) || ctx->store.n_layers == 1));
     ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
                       dyn ? ctx->d_ticket : nullptr,
-                      dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr};
+                      dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
+                      extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
+                      extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0};
     cudaError_t e = ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
@@ -429,18 +432,35 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
     });
 }
 
-ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
-                   const uint32_t *d_event_ids, double *d_ylt, uint64_t ylt_ld, uint32_t flags)
+ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
+                           const uint32_t *d_event_ids, const ara_outputs *out, uint32_t flags)
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
         if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
+        if (!out) return fail(ctx, ARA_ERR_ARG, "outputs is NULL");
         if (n_trials == 0) return ARA_OK;
-        if (!d_trial_offsets || !d_event_ids || !d_ylt)
+        if (!d_trial_offsets || !d_event_ids || !out->ylt)
             return fail(ctx, ARA_ERR_ARG, "device pointer is NULL");
-        const uint64_t ld = ylt_ld ? ylt_ld : n_trials;
-        if (ld < n_trials) return fail(ctx, ARA_ERR_ARG, "ylt_ld %llu < n_trials", (unsigned long long)ld);
+        ara_outputs o = *out;
+        if (!o.ylt_ld) o.ylt_ld = n_trials;
+        if (!o.max_occ_ld) o.max_occ_ld = n_trials;
+        if (o.ylt_ld < n_trials || (o.max_occ && o.max_occ_ld < n_trials))
+            return fail(ctx, ARA_ERR_ARG, "leading dimension < n_trials");
+        if (o.event_inc) {  // needs the YET's event count: two 8-byte reads of the offsets
+            uint64_t ends[2];
+            ARA_CUDA(ctx, cudaMemcpyAsync(&ends[0], d_trial_offsets, 8, cudaMemcpyDeviceToHost,
+                                          ctx->stream));
+            ARA_CUDA(ctx, cudaMemcpyAsync(&ends[1], d_trial_offsets + n_trials, 8,
+                                          cudaMemcpyDeviceToHost, ctx->stream));
+            ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            const uint64_t n_ev = ends[1] - ends[0];
+            if (!o.event_inc_ld) o.event_inc_ld = n_ev;
+            if (o.event_inc_ld < n_ev)
+                return fail(ctx, ARA_ERR_ARG, "event_inc_ld %llu < %llu events",
+                            (unsigned long long)o.event_inc_ld, (unsigned long long)n_ev);
+        }
         if (flags & ARA_RUN_VALIDATE) {
             ara_status s = check_device_error(ctx);  // report earlier deferred errors first
             if (s != ARA_OK) return s;
@@ -451,11 +471,20 @@ ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offs
             s = check_device_error(ctx);
             if (s != ARA_OK) return s;
         }
-        ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, d_ylt, ld, flags);
+        const bool extra = o.max_occ || o.event_inc;
+        ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, o.ylt, o.ylt_ld,
+                                     flags, extra ? &o : nullptr);
         if (s != ARA_OK) return s;
         if (flags & (ARA_RUN_SYNC | ARA_RUN_VALIDATE)) return check_device_error(ctx);
         return ARA_OK;
     });
+}
+
+ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
+                   const uint32_t *d_event_ids, double *d_ylt, uint64_t ylt_ld, uint32_t flags)
+{
+    const ara_outputs o{d_ylt, ylt_ld, nullptr, 0, nullptr, 0};
+    return ara_run_outputs(ctx, n_trials, d_trial_offsets, d_event_ids, &o, flags);
 }
 
 ara_status ara_synchronize(ara_ctx *ctx)

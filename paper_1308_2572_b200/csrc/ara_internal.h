@@ -80,6 +80,10 @@ struct ScanLaunch {
     uint32_t *err;            // device error word (bit 0: id out of range)
     unsigned long long *counter;  // dynamic ticket counter (NULL: static assignment)
     unsigned int *done;           // finished-block counter (resets `counter`)
+    double *max_occ;              // F4: [n_layers][max_occ_ld] or NULL
+    uint64_t max_occ_ld;
+    double *event_inc;            // F4: [n_layers][event_inc_ld] or NULL (YET positions)
+    uint64_t event_inc_ld;
 };
 
 // scan.cu

@@ -92,7 +92,8 @@ __device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&r
                                            const double (&ret)[4 * CH],
                                            const double (&lim)[4 * CH], uint32_t gmask,
                                            double occ_ret, double occ_lim, double agg_ret,
-                                           double agg_lim, double &S, double &Cprev, double &lr)
+                                           double agg_lim, double &S, double &Cprev, double &lr,
+                                           double &oc_out, double &inc_out)
 {
     constexpr int NCOL = 4 * CH;
     // A4, line 9 on this lane's columns: min(max(x*rate - ret, 0), lim)
@@ -120,8 +121,23 @@ __device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&r
     const double oc = dmin(dmax0(__dsub_rn(part, occ_ret)), occ_lim);  // line 16
     S = __dadd_rn(S, oc);                                                // line 19
     const double Cd = dmin(dmax0(__dsub_rn(S, agg_ret)), agg_lim);       // line 22
-    lr = __dadd_rn(lr, __dsub_rn(Cd, Cprev));                            // lines 25, 28
+    const double inc = __dsub_rn(Cd, Cprev);                             // line 25
+    lr = __dadd_rn(lr, inc);                                             // line 28
     Cprev = Cd;
+    oc_out = oc;
+    inc_out = inc;
+}
+
+// F4 outputs of one event (X: compiled in only when requested): the trial's maximum
+// occurrence loss and the event's incremental aggregate loss at its YET position.
+template <bool X>
+__device__ __forceinline__ void event_out(double oc, double inc, double &max_oc, double *inc_row,
+                                          uint64_t pos, bool writer)
+{
+    if (X) {
+        max_oc = (max_oc < oc) ? oc : max_oc;
+        if (inc_row && writer) inc_row[pos] = inc;
+    }
 }
 
 template <int CH>
@@ -133,7 +149,7 @@ __device__ __forceinline__ void gather(const double *__restrict__ my_rows, uint3
     for (int i = 0; i < CH; ++i) load_row_chunk(p + 4 * i, r[i]);
 }
 
-template <int G, int CH, int MINB>
+template <int G, int CH, int MINB, bool X>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                 const double *__restrict__ rows, const LayerTermsDev *__restrict__ terms,
@@ -160,6 +176,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     double occ_ret = 0, occ_lim = 0, agg_ret = 0, agg_lim = 0;
     const double *__restrict__ my_rows = rows;
     double *ylt_row = s.ylt;
+    double *mo_row = nullptr, *inc_row = nullptr;  // F4 outputs (X only)
     uint32_t cur_layer = 0xffffffffu;
 
     const uint64_t base = s.offsets[0];
@@ -182,6 +199,10 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             agg_lim = T.agg_lim;
             my_rows = rows + (size_t)layer * W + NCOL * c;
             ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
+            if (X) {
+                mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
+                inc_row = s.event_inc ? s.event_inc + (size_t)layer * s.event_inc_ld : nullptr;
+            }
             cur_layer = layer;
         }
         const uint64_t beg = s.offsets[t] - base;
@@ -189,13 +210,16 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         const uint32_t *ev = s.ids + beg;
         const uint32_t *const ev_end = ev + k;
         double S = 0.0, Cprev = 0.0, lr = 0.0;  // lines 19, 25 (C_0 = 0), 28
+        double max_oc = 0.0, oc, inc;           // F4
+        const bool writer = c == G - 1;
 
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Row4 r[CH];
             gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
             event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
-                              Cprev, lr);
+                              Cprev, lr, oc, inc);
+            event_out<X>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
         // body: chunks of 8 events.  Pipeline per group: the ids of chunk i+1 are in flight
@@ -223,11 +247,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     Row4 rb[CH];
                     gather<CH>(my_rows, row_stride, pin(idx1, S), rb);
                     event_step<G, CH>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
-                                      agg_lim, S, Cprev, lr);
+                                      agg_lim, S, Cprev, lr, oc, inc);
+                    event_out<X>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                     uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
                     gather<CH>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
                     event_step<G, CH>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
-                                      agg_lim, S, Cprev, lr);
+                                      agg_lim, S, Cprev, lr, oc, inc);
+                    event_out<X>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1, writer);
                     idx1 = idx3;
                 }
 #pragma unroll
@@ -241,10 +267,14 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             Row4 r[CH];
             gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
             event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
-                              Cprev, lr);
+                              Cprev, lr, oc, inc);
+            event_out<X>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
-        if (c == G - 1) ylt_row[t] = lr;  // A8
+        if (writer) {
+            ylt_row[t] = lr;  // A8
+            if (X && mo_row) mo_row[t] = max_oc;
+        }
         if (s.counter) {
             uint64_t next = 0;
             if (c == 0) next = groups + atomicAdd(s.counter, 1ull);
@@ -287,14 +317,14 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
     if (e) atomicOr(err, e);
 }
 
-template <int G, int CH, int MINB = 1>
+template <int G, int CH, int MINB = 1, bool X = false>
 cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
 {
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, scan_kernel<G, CH, MINB>, kScanThreads, 0);
+            &occ, scan_kernel<G, CH, MINB, X>, kScanThreads, 0);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -317,7 +347,7 @@ cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
         blocks = (blocks + lcm - 1) / lcm * lcm;
     if (blocks > max_blocks) blocks = max_blocks;
-    scan_kernel<G, CH, MINB><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
+    scan_kernel<G, CH, MINB, X><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
         s, st.d_map, st.d_rows, st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
@@ -329,6 +359,17 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
+    if (s.max_occ || s.event_inc) {  // F4 outputs: default decomposition only
+        switch (st.width) {
+            case 4: return launch_gc<1, 1, 1, true>(st, s, sm_count, stream);
+            case 8: return launch_gc<2, 1, 1, true>(st, s, sm_count, stream);
+            case 16: return launch_gc<2, 2, 1, true>(st, s, sm_count, stream);
+            case 32: return launch_gc<4, 2, 1, true>(st, s, sm_count, stream);
+            case 48: return launch_gc<4, 3, 1, true>(st, s, sm_count, stream);
+            case 64: return launch_gc<4, 4, 1, true>(st, s, sm_count, stream);
+            default: --*launches; return cudaErrorInvalidValue;
+        }
+    }
     const ScanShape sh = scan_shape_for_width(st.width, st.group_override);
     switch (sh.G * 16 + sh.CH) {
         case 1 * 16 + 1: return launch_gc<1, 1>(st, s, sm_count, stream);

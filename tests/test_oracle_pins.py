@@ -393,3 +393,34 @@ def test_separate_rounding_no_fma():
         assert got == want
         n_diff_from_exact += float(Fraction(xi) * Fraction(ri) - Fraction(ti)) != got
     assert n_diff_from_exact > 1000  # the test data does exercise the double rounding
+
+
+# --------------------------------------------------------------------------- F4 outputs
+def test_event_increments_and_max_occurrence_brute_force():
+    """F4 outputs, exactly on integer/dyadic data: the per-event increments of lines 24-26 are
+    the erosion |[S_{d-1}, S_d] cap [AggR, AggR+AggL]| of each occurrence, they sum to lr
+    (line 28), and max_occ is the largest occurrence loss xl(lo_d; OccR, OccL) of the trial
+    (0 for an empty trial) -- the quantity whose distribution is the OEP curve."""
+    cat, elts, fin, occ, agg = list(_exhaustive_cases())[1]
+    trials = [list(t) for k in range(4) for t in itertools.product(range(1, cat + 1), repeat=k)]
+    ds = make_dataset(cat, [{"records": sorted(e.items()), "fin": f} for e, f in zip(elts, fin)],
+                      [{"elts": list(range(len(elts))), "terms": (*occ, *agg)}], trials)
+    ylt, mo, inc = oracle.run_analysis(ds, outputs=True)
+    agg_hi = INF if agg[1] == INF else Fraction(agg[0]) + Fraction(agg[1])
+    for t, ev in enumerate(trials):
+        pos = int(ds.trial_offsets[t])
+        s_prev, best = Fraction(0), Fraction(0)
+        for d, e in enumerate(ev):
+            lo = sum((xl(Fraction(elts[j].get(e, 0)) * Fraction(fin[j][0]), Fraction(fin[j][1]),
+                         fin[j][2] if fin[j][2] == INF else Fraction(fin[j][2]))
+                      for j in range(len(elts))), Fraction(0))
+            oc = xl(lo, Fraction(occ[0]), occ[1] if occ[1] == INF else Fraction(occ[1]))
+            assert inc[0, pos + d] == seg(s_prev, s_prev + oc, Fraction(agg[0]), agg_hi)
+            s_prev += oc
+            best = max(best, oc)
+        assert mo[0, t] == best
+        assert ylt[0, t] == math.fsum(inc[0, pos:pos + len(ev)])
+    # selection keeps event positions of the whole YET
+    sel = np.array([5, 2], np.uint64)
+    y2, m2, i2 = oracle.run_analysis(ds, selection=sel, outputs=True)
+    assert np.array_equal(m2[0], mo[0, [5, 2]])

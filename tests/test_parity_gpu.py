@@ -376,3 +376,34 @@ def test_dynamic_balance_scheduling(stream, preset, k):
     assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
     assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_BALANCE), want)
     ctx.close()
+
+
+@pytest.mark.parametrize("preset,kw", [("tiny", dict(n_trials=700, k_min=0, k_max=45)),
+                                       ("portfolio", dict(n_trials=300, k_min=20, k_max=90)),
+                                       ("medium", dict(n_trials=600, k_min=1000, k_max=1000))])
+def test_f4_outputs(stream, preset, kw):
+    """F4: per-trial maximum occurrence loss (OEP basis) and per-event incremental aggregate
+    losses (lines 24-26) from the same pass, bit-identical to the oracle; the YLT is unchanged
+    by requesting them; OEP PML/TVaR through ara_metrics on a max_occ row."""
+    ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
+    y_o, mo_o, inc_o = oracle.run_analysis(ds, n_threads=8, outputs=True)
+    ctx = make_ctx(ds, stream)
+    L, n = ds.n_layers, ds.n_trials
+    n_ev = int(ds.trial_offsets[-1])
+    ylt = torch.full((L, n), float("nan"), dtype=torch.float64, device=DEV)
+    mo = torch.full((L, n), float("nan"), dtype=torch.float64, device=DEV)
+    inc = torch.full((L, n_ev + 3), float("nan"), dtype=torch.float64, device=DEV)
+    ctx.ara_run_outputs(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, mo, inc,
+                        flags=ara.ARA_RUN_SYNC, event_inc_ld=n_ev + 3)
+    assert_bit_identical(ylt.cpu().numpy(), y_o)
+    assert_bit_identical(mo.cpu().numpy(), mo_o)
+    got_inc = inc.cpu().numpy()
+    assert_bit_identical(got_inc[:, :n_ev], inc_o)
+    assert np.isnan(got_inc[:, n_ev:]).all()
+    pml, tvar = ctx.ara_metrics(mo[0], P_RP)
+    opml, otvar = oracle.metrics(mo_o[0], P_RP)
+    assert np.array_equal(pml, opml) and np.allclose(tvar, otvar, rtol=1e-9, atol=0)
+    with pytest.raises(ara.AraError, match="ARA_ERR_ARG"):
+        ctx.ara_run_outputs(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, mo,
+                            inc, event_inc_ld=max(n_ev - 1, 1))
+    ctx.close()
