@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="headline", choices=sorted(datagen.PRESETS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="64: the graded fp64 path; 32: the paper's float variant (F3)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -237,6 +239,7 @@ def main():
     d_ylt_full = torch.empty((L, spec.n_trials), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     ctx = ara.Context(local, stream)
+    ctx.ara_set_precision(args.precision)
     ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
     t_store = time.perf_counter()
     ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
@@ -301,7 +304,8 @@ def main():
     E = spec.elts_per_layer
     # one fused launch covers all layers: the id stream and offsets are read once, every layer's
     # E-wide fp64 row segment is gathered per event, every layer's YLT entry is written
-    bytes_alg = n_ev * (4 + 8 * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
+    vb = args.precision // 8  # bytes per stored loss
+    bytes_alg = n_ev * (4 + vb * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
     peak, peak_src = measured_peak()
     achieved = bytes_alg / (scan_ms * 1e-3) / 1e9
     traffic = None
@@ -355,7 +359,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (datagen SplitMix64, seed 1308; truncated-Pareto ELT losses)",
             "config": {"workload": workload_name(spec), "layers": L, "elts_per_layer": E,
                        "trials": spec.n_trials, "events_per_trial": spec.k_min,
@@ -369,7 +374,7 @@ def main():
                          "kernel": f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})",
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
-                         "bytes_model": "n*k*(4 + 8*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
+                         "bytes_model": f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
                                         "segment per event, YLT, offsets (north-star accounting)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -93,6 +93,16 @@ const char *ara_status_string(ara_status s);
  * the caller keeps ownership of the stream.  *out receives the context. */
 ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out);
 
+/*
+ * Arithmetic precision of the store and the scan: 64 (default: fp64, the graded path, bit-
+ * identical to the fp64 oracle) or 32 (the paper's optimisation "changing the double variables to
+ * float variables"): losses and terms are rounded to float once
+ * when the store is built, every step of Algorithm 1 runs in float in the same order, and the
+ * YLT is widened to double.  Invalidates the layers: call before ara_set_layers.
+ * Errors: ARA_ERR_ARG (bits not 32 or 64).
+ */
+ara_status ara_set_precision(ara_ctx *ctx, uint32_t bits);
+
 /* Change the stream of an existing context (caller-owned cudaStream_t or NULL). */
 ara_status ara_set_stream(ara_ctx *ctx, void *cuda_stream);
 

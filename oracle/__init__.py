@@ -16,6 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_INC = os.path.join(_HERE, "alg1.inc")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 # -ffp-contract=off: products and differences are rounded separately (no FMA), as the
@@ -25,7 +26,8 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-st
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C, no CUDA)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(_INC)):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lpthread", "-lm"])
         os.replace(tmp, _LIB)
@@ -56,6 +58,13 @@ def lib() -> ctypes.CDLL:
         L.oracle_run_analysis_ex.argtypes = [u32, u32, p, p, p, p, u32, p, p, p, u64, p, p,
                                              u64, p, p, p, p, ctypes.c_int]
         L.oracle_run_analysis_ex.restype = ctypes.c_int
+        L.oracle_run_analysis_f32.argtypes = L.oracle_run_analysis_ex.argtypes
+        L.oracle_run_analysis_f32.restype = ctypes.c_int
+        f = ctypes.c_float
+        L.oracle_apply_financial_terms_f32.argtypes = [f, f, f, f]
+        L.oracle_apply_financial_terms_f32.restype = f
+        L.oracle_apply_occurrence_terms_f32.argtypes = [f, f, f]
+        L.oracle_apply_occurrence_terms_f32.restype = f
         L.oracle_metrics.argtypes = [p, u64, u32, p, p, p]
         L.oracle_metrics.restype = ctypes.c_int
         _lib = L
@@ -69,6 +78,11 @@ def _ptr(a: np.ndarray) -> int:
 def apply_financial_terms(x: float, rate: float, retention: float, limit: float) -> float:
     """Alg. 1 line 9 under reading R1."""
     return lib().oracle_apply_financial_terms(x, rate, retention, limit)
+
+
+def apply_financial_terms_f32(x, rate, retention, limit) -> float:
+    """Line 9 in float arithmetic (F3)."""
+    return lib().oracle_apply_financial_terms_f32(x, rate, retention, limit)
 
 
 def apply_occurrence_terms(lo: float, occ_retention: float, occ_limit: float) -> float:
@@ -99,7 +113,7 @@ def build_dat(catalogue_size: int, event_ids, losses) -> np.ndarray:
 
 
 def run_analysis(ds, selection: Optional[np.ndarray] = None, n_threads: int = 1,
-                 trial_offsets=None, events=None, outputs: bool = False):
+                 trial_offsets=None, events=None, outputs: bool = False, precision: int = 64):
     """YLT[n_layers][n] of Algorithm 1.
 
     ``ds`` carries numpy arrays: catalogue_size, rec_offsets, rec_event_ids, rec_losses,
@@ -126,7 +140,10 @@ def run_analysis(ds, selection: Optional[np.ndarray] = None, n_threads: int = 1,
     inc = np.zeros((n_layers, max(n_ev, 1))) if outputs else None
     if n_layers == 0 or n_out == 0:
         return (ylt, mo, inc[:, :n_ev]) if outputs else ylt
-    st = lib().oracle_run_analysis_ex(
+    fn = lib().oracle_run_analysis_ex if precision == 64 else lib().oracle_run_analysis_f32
+    if precision not in (32, 64):
+        raise ValueError("precision must be 32 or 64")
+    st = fn(
         int(ds.catalogue_size), rec_off.shape[0] - 1, _ptr(rec_off), _ptr(rec_ids),
         _ptr(rec_ls), _ptr(fin), n_layers, _ptr(lt), _ptr(eo),
         _ptr(ei) if ei.size else None, n_trials, _ptr(to),

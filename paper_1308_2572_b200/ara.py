@@ -27,7 +27,7 @@ ARA_MAX_ELTS_PER_LAYER = 64
 ARA_MAX_P = 32
 
 # Every symbol include/ara.h declares (tests check the library exports all of them).
-EXPORTS = ["ara_status_string", "ara_create", "ara_set_stream", "ara_destroy", "ara_last_error",
+EXPORTS = ["ara_status_string", "ara_create", "ara_set_precision", "ara_set_stream", "ara_destroy", "ara_last_error",
            "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
            "ara_synchronize",
            "ara_metrics", "ara_metrics_host", "ara_get_info", "ara_layer_store_shape",
@@ -80,6 +80,7 @@ def _load() -> ctypes.CDLL:
         "ara_status_string": ([i32], ctypes.c_char_p),
         "ara_create": ([i32, p, ctypes.POINTER(p)], i32),
         "ara_set_stream": ([p, p], i32),
+        "ara_set_precision": ([p, u32], i32),
         "ara_destroy": ([p], None),
         "ara_last_error": ([p], ctypes.c_char_p),
         "ara_load_elts": ([p, u32, u32, p, p, p, p], i32),
@@ -169,6 +170,9 @@ class Context:
         self.close()
 
     # ------------------------------------------------------------------ calls
+    def ara_set_precision(self, bits: int):
+        self._check(lib().ara_set_precision(self._ptr, int(bits)))
+
     def ara_set_stream(self, stream):
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
         self._check(lib().ara_set_stream(self._ptr, handle))

@@ -41,6 +41,7 @@ struct ara_ctx {
     uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
     unsigned long long *d_ticket = nullptr;  // dynamic scheduling: ticket + done counters
     int sched = 0;              // 0 auto, 1 static, 2 dynamic (env ARA_SCAN_SCHED)
+    int bits = 64;              // store / arithmetic precision (ara_set_precision)
     uint32_t *h_err = nullptr;  // pinned mirror
     uint64_t launches = 0;
     ara::MetricsScratch metrics;
@@ -176,6 +177,43 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     return ARA_OK;
 }
 
+// Event-major rows and per-layer terms of the store in precision R (double: bit copies of the
+// losses; float: each value rounded to nearest once, F3).  Layer l's columns sit at l * W.
+template <typename R>
+void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vector<uint32_t> &map,
+                const ara_layer_terms *terms, const uint32_t *elt_offsets,
+                const uint32_t *elt_index, std::vector<char> &rows_buf,
+                std::vector<char> &terms_buf)
+{
+    const uint32_t n_layers = st.n_layers, W = st.width;
+    const size_t stride = (size_t)n_layers * W;
+    rows_buf.assign((size_t)(st.n_union + 1) * stride * sizeof(R), 0);
+    terms_buf.assign((size_t)n_layers * sizeof(ara::LayerTermsT<R>), 0);
+    R *rows = (R *)rows_buf.data();
+    ara::LayerTermsT<R> *lt = (ara::LayerTermsT<R> *)terms_buf.data();
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        const uint32_t E = st.n_cols[l];
+        for (uint32_t c = 0; c < E; ++c) {
+            const uint32_t j = elt_index[elt_offsets[l] + c];
+            for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
+                rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W + c] =
+                    (R)ctx->rec_losses[r];
+            lt[l].rate[c] = (R)ctx->fin[j].rate;
+            lt[l].ret[c] = (R)ctx->fin[j].retention;
+            lt[l].lim[c] = (R)ctx->fin[j].limit;
+        }
+        for (uint32_t c = E; c < ara::kMaxCols; ++c) {  // neutral padding columns
+            lt[l].rate[c] = (R)1;
+            lt[l].ret[c] = (R)0;
+            lt[l].lim[c] = (R)INFINITY;
+        }
+        lt[l].occ_ret = (R)terms[l].occ_retention;
+        lt[l].occ_lim = (R)terms[l].occ_limit;
+        lt[l].agg_ret = (R)terms[l].agg_retention;
+        lt[l].agg_lim = (R)terms[l].agg_limit;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -228,6 +266,20 @@ ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
     }
     *out = ctx;
     return ARA_OK;
+}
+
+ara_status ara_set_precision(ara_ctx *ctx, uint32_t bits)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (bits != 32 && bits != 64)
+            return fail(ctx, ARA_ERR_ARG, "precision %u bits: 32 or 64 expected", bits);
+        if ((int)bits != ctx->bits) {
+            ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            free_layers(ctx);
+            ctx->bits = (int)bits;
+        }
+        return ARA_OK;
+    });
 }
 
 ara_status ara_set_stream(ara_ctx *ctx, void *cuda_stream)
@@ -369,8 +421,9 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
             st.n_cols.push_back(elt_offsets[l + 1] - elt_offsets[l]);
             maxE = std::max(maxE, st.n_cols.back());
         }
-        const uint32_t W = ara::row_width_for(maxE);
+        const uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);
         st.width = W;
+        st.bits = ctx->bits;
         if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
         std::vector<uint32_t> map((size_t)C + 1, 0u);
@@ -388,40 +441,23 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         std::sort(uni.begin(), uni.end());
         st.n_union = (uint32_t)uni.size();
         for (uint32_t u = 0; u < st.n_union; ++u) map[uni[u]] = u + 1;
-        const size_t stride = (size_t)n_layers * W;
-        std::vector<double> rows((size_t)(st.n_union + 1) * stride, 0.0);
-        std::vector<ara::LayerTermsDev> lt(n_layers);
-        for (uint32_t l = 0; l < n_layers; ++l) {
-            const uint32_t E = st.n_cols[l];
-            for (uint32_t c = 0; c < E; ++c) {
-                const uint32_t j = elt_index[elt_offsets[l] + c];
-                for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)  // bit copy
-                    rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W + c] =
-                        ctx->rec_losses[r];
-                lt[l].rate[c] = ctx->fin[j].rate;
-                lt[l].ret[c] = ctx->fin[j].retention;
-                lt[l].lim[c] = ctx->fin[j].limit;
-            }
-            for (uint32_t c = E; c < ara::kMaxCols; ++c) {  // neutral padding columns
-                lt[l].rate[c] = 1.0;
-                lt[l].ret[c] = 0.0;
-                lt[l].lim[c] = INFINITY;
-            }
-            lt[l].occ_ret = terms[l].occ_retention;
-            lt[l].occ_lim = terms[l].occ_limit;
-            lt[l].agg_ret = terms[l].agg_retention;
-            lt[l].agg_lim = terms[l].agg_limit;
-        }
-        const size_t map_bytes = ((size_t)C + 1) * 4, row_bytes = rows.size() * 8,
-                     term_bytes = lt.size() * sizeof(ara::LayerTermsDev);
+        size_t row_bytes = 0, term_bytes = 0;
+        std::vector<char> rows_buf, terms_buf;
+        if (ctx->bits == 32)
+            build_rows<float>(ctx, st, map, terms, elt_offsets, elt_index, rows_buf, terms_buf);
+        else
+            build_rows<double>(ctx, st, map, terms, elt_offsets, elt_index, rows_buf, terms_buf);
+        row_bytes = rows_buf.size();
+        term_bytes = terms_buf.size();
+        const size_t map_bytes = ((size_t)C + 1) * 4;
         cudaError_t e = cudaMalloc(&st.d_map, map_bytes);
         if (e == cudaSuccess) e = cudaMalloc(&st.d_rows, row_bytes);
         if (e == cudaSuccess) e = cudaMalloc(&st.d_terms, term_bytes);
         if (e == cudaSuccess) e = cudaMemcpy(st.d_map, map.data(), map_bytes, cudaMemcpyHostToDevice);
         if (e == cudaSuccess)
-            e = cudaMemcpy(st.d_rows, rows.data(), row_bytes, cudaMemcpyHostToDevice);
+            e = cudaMemcpy(st.d_rows, rows_buf.data(), row_bytes, cudaMemcpyHostToDevice);
         if (e == cudaSuccess)
-            e = cudaMemcpy(st.d_terms, lt.data(), term_bytes, cudaMemcpyHostToDevice);
+            e = cudaMemcpy(st.d_terms, terms_buf.data(), term_bytes, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             free_layers(ctx);
             return cuda_fail(ctx, e, "device ELT store");
@@ -658,11 +694,18 @@ ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, doubl
         ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         if (h_map)
             ARA_CUDA(ctx, cudaMemcpy(h_map, st.d_map, ((size_t)ctx->C + 1) * 4, cudaMemcpyDeviceToHost));
-        if (h_rows)  // this layer's W columns of every union row
-            ARA_CUDA(ctx, cudaMemcpy2D(h_rows, (size_t)st.width * 8,
-                                       st.d_rows + (size_t)layer * st.width,
-                                       (size_t)st.n_layers * st.width * 8, (size_t)st.width * 8,
+        if (h_rows) {  // this layer's W columns of every union row, widened to double
+            const size_t es = st.bits == 32 ? 4 : 8;
+            std::vector<char> tmp((size_t)(st.n_union + 1) * st.width * es);
+            ARA_CUDA(ctx, cudaMemcpy2D(tmp.data(), (size_t)st.width * es,
+                                       (const char *)st.d_rows + (size_t)layer * st.width * es,
+                                       (size_t)st.n_layers * st.width * es, (size_t)st.width * es,
                                        st.n_union + 1, cudaMemcpyDeviceToHost));
+            const size_t cnt = (size_t)(st.n_union + 1) * st.width;
+            for (size_t i = 0; i < cnt; ++i)
+                h_rows[i] = st.bits == 32 ? (double)((const float *)tmp.data())[i]
+                                          : ((const double *)tmp.data())[i];
+        }
         return ARA_OK;
     });
 }

@@ -18,12 +18,14 @@ constexpr int kMaxCols = ARA_MAX_ELTS_PER_LAYER;  // row width limit W (doubles)
 // financial terms and its layer's occurrence / aggregate terms into registers at kernel start.
 // Padded columns j >= E carry the neutral terms (rate 1, retention 0, limit +inf) and zero
 // losses, so F_j = +0 and lo + (+0) = lo exactly (reading R12).
-struct LayerTermsDev {
-    double rate[kMaxCols];
-    double ret[kMaxCols];
-    double lim[kMaxCols];
-    double occ_ret, occ_lim, agg_ret, agg_lim;
+template <typename R>
+struct LayerTermsT {
+    R rate[kMaxCols];
+    R ret[kMaxCols];
+    R lim[kMaxCols];
+    R occ_ret, occ_lim, agg_ret, agg_lim;
 };
+using LayerTermsDev = LayerTermsT<double>;
 
 // Scan decomposition for a row width: G lanes per trial, each owning CH 32-byte chunks
 // (4 doubles each), W = 4 * G * CH.  The paper's 15-16 ELT layers give W = 16 and G = 2: a
@@ -34,7 +36,15 @@ struct ScanShape {
     int G, CH;
 };
 
-// Row width (doubles) of the event-major store for a layer of E ELTs.
+// Row width (elements) of the event-major store for a layer of E ELTs: whole 32-byte chunks.
+// fp32 store (F3): 8 floats per chunk -> 8, 16, 32 or 64.
+inline uint32_t row_width_for_f32(uint32_t E)
+{
+    const uint32_t nc = (E + 7) / 8;
+    return nc <= 1 ? 8 : nc == 2 ? 16 : nc <= 4 ? 32 : 64;
+}
+
+// fp64 store: 4 doubles per chunk.
 inline uint32_t row_width_for(uint32_t E)
 {
     const uint32_t nc = (E + 3) / 4;  // 32-byte chunks needed
@@ -61,13 +71,14 @@ inline ScanShape scan_shape_for_width(uint32_t W, int override_g)
 struct DeviceStore {
     uint32_t n_layers = 0;
     uint32_t n_union = 0;        // U: distinct events over all layers' ELTs
-    uint32_t width = 0;          // W = row_width_for(max E) doubles per layer
+    uint32_t width = 0;          // W = row width (elements) per layer
+    int bits = 64;               // 64: fp64 store and arithmetic; 32: fp32 (F3)
     std::vector<uint32_t> n_cols;  // E of each layer
     int group_override = 0;      // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
     int min_blocks = 0;          // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
-    double *d_rows = nullptr;    // [(U+1) * n_layers * W], row 0 zero
-    LayerTermsDev *d_terms = nullptr;  // [n_layers]
+    void *d_rows = nullptr;      // [(U+1) * n_layers * W] double or float, row 0 zero
+    void *d_terms = nullptr;     // [n_layers] LayerTermsT<double or float>
 };
 
 struct ScanLaunch {

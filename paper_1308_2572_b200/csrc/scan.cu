@@ -31,16 +31,35 @@ namespace {
 
 constexpr int kScanThreads = 128;  // 4 warps: fine occupancy steps for 80-170 registers
 
-struct Row4 {
-    double v[4];
+// One 32-byte chunk of a row: 4 doubles (fp64 store) or 8 floats (fp32 store, F3).
+template <typename R>
+struct Chunk {
+    static constexpr int N = 32 / (int)sizeof(R);
+    R v[N];
 };
 
-__device__ __forceinline__ void load_row_chunk(const double *p, Row4 &r)
+__device__ __forceinline__ void load_row_chunk(const double *p, Chunk<double> &r)
 {
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
         : "l"(p));
 }
+
+__device__ __forceinline__ void load_row_chunk(const float *p, Chunk<float> &r)
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+          "=f"(r.v[6]), "=f"(r.v[7])
+        : "l"(p));
+}
+
+// Separately rounded arithmetic in the store's precision (no FMA contraction).
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
 
 __device__ __forceinline__ void load_ids8(const uint32_t *p, uint32_t (&v)[8])
 {
@@ -65,8 +84,10 @@ __device__ __forceinline__ uint32_t load_map(const uint32_t *p)
 }
 
 // min(x, y) = (y < x ? y : x); max(x, 0) = (x < 0 ? 0 : x)   (the oracle's definitions)
-__device__ __forceinline__ double dmin(double x, double y) { return (y < x) ? y : x; }
-__device__ __forceinline__ double dmax0(double x) { return (x < 0.0) ? 0.0 : x; }
+template <typename R>
+__device__ __forceinline__ R dmin(R x, R y) { return (y < x) ? y : x; }
+template <typename R>
+__device__ __forceinline__ R dmax0(R x) { return (x < R(0)) ? R(0) : x; }
 
 __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, uint32_t id,
                                               uint32_t C, bool &bad)
@@ -86,43 +107,50 @@ __device__ __forceinline__ uint32_t pin(uint32_t idx, double S)
     return min(idx, 0xffffffffu - sbit);
 }
 
-// A2-A8 for one event with its row chunks in r[] (see the file comment).
-template <int G, int CH>
-__device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&rate)[4 * CH],
-                                           const double (&ret)[4 * CH],
-                                           const double (&lim)[4 * CH], uint32_t gmask,
-                                           double occ_ret, double occ_lim, double agg_ret,
-                                           double agg_lim, double &S, double &Cprev, double &lr,
-                                           double &oc_out, double &inc_out)
+__device__ __forceinline__ uint32_t pin(uint32_t idx, float S)
 {
-    constexpr int NCOL = 4 * CH;
+    const uint32_t sbit = __float_as_uint(S) >> 31;
+    return min(idx, 0xffffffffu - sbit);
+}
+
+// A2-A8 for one event with its row chunks in r[] (see the file comment).
+template <int G, int CH, typename R>
+__device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
+                                           const R (&rate)[Chunk<R>::N * CH],
+                                           const R (&ret)[Chunk<R>::N * CH],
+                                           const R (&lim)[Chunk<R>::N * CH], uint32_t gmask,
+                                           R occ_ret, R occ_lim, R agg_ret, R agg_lim, R &S,
+                                           R &Cprev, R &lr, R &oc_out, R &inc_out)
+{
+    constexpr int PER = Chunk<R>::N;
+    constexpr int NCOL = PER * CH;
     // A4, line 9 on this lane's columns: min(max(x*rate - ret, 0), lim)
-    double f[NCOL];
+    R f[NCOL];
 #pragma unroll
     for (int i = 0; i < CH; ++i)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = 4 * i + q;
-            const double l = __dsub_rn(__dmul_rn(r[i].v[q], rate[j]), ret[j]);
+        for (int q = 0; q < PER; ++q) {
+            const int j = PER * i + q;
+            const R l = rsub(rmul(r[i].v[q], rate[j]), ret[j]);
             f[j] = dmin(dmax0(l), lim[j]);
         }
     // lines 11-13: lo = ((0 + F_0) + F_1) + ... through the group in column order
-    double part = 0.0;
+    R part = R(0);
 #pragma unroll
-    for (int j = 0; j < NCOL; ++j) part = __dadd_rn(part, f[j]);
+    for (int j = 0; j < NCOL; ++j) part = radd(part, f[j]);
 #pragma unroll
     for (int h = 1; h < G; ++h) {
-        double x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
+        R x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
 #pragma unroll
-        for (int j = 0; j < NCOL; ++j) x = __dadd_rn(x, f[j]);
+        for (int j = 0; j < NCOL; ++j) x = radd(x, f[j]);
         part = x;  // valid in lane h after hop h
     }
     // A5-A7 (valid in lane G-1)
-    const double oc = dmin(dmax0(__dsub_rn(part, occ_ret)), occ_lim);  // line 16
-    S = __dadd_rn(S, oc);                                                // line 19
-    const double Cd = dmin(dmax0(__dsub_rn(S, agg_ret)), agg_lim);       // line 22
-    const double inc = __dsub_rn(Cd, Cprev);                             // line 25
-    lr = __dadd_rn(lr, inc);                                             // line 28
+    const R oc = dmin(dmax0(rsub(part, occ_ret)), occ_lim);  // line 16
+    S = radd(S, oc);                                          // line 19
+    const R Cd = dmin(dmax0(rsub(S, agg_ret)), agg_lim);      // line 22
+    const R inc = rsub(Cd, Cprev);                            // line 25
+    lr = radd(lr, inc);                                       // line 28
     Cprev = Cd;
     oc_out = oc;
     inc_out = inc;
@@ -130,33 +158,34 @@ __device__ __forceinline__ void event_step(const Row4 (&r)[CH], const double (&r
 
 // F4 outputs of one event (X: compiled in only when requested): the trial's maximum
 // occurrence loss and the event's incremental aggregate loss at its YET position.
-template <bool X>
-__device__ __forceinline__ void event_out(double oc, double inc, double &max_oc, double *inc_row,
-                                          uint64_t pos, bool writer)
+template <bool X, typename R>
+__device__ __forceinline__ void event_out(R oc, R inc, R &max_oc, double *inc_row, uint64_t pos,
+                                          bool writer)
 {
     if (X) {
         max_oc = (max_oc < oc) ? oc : max_oc;
-        if (inc_row && writer) inc_row[pos] = inc;
+        if (inc_row && writer) inc_row[pos] = (double)inc;
     }
 }
 
-template <int CH>
-__device__ __forceinline__ void gather(const double *__restrict__ my_rows, uint32_t stride,
-                                       uint32_t idx, Row4 (&r)[CH])
+template <int CH, typename R>
+__device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t stride,
+                                       uint32_t idx, Chunk<R> (&r)[CH])
 {
-    const double *p = my_rows + (size_t)idx * stride;
+    const R *p = my_rows + (size_t)idx * stride;
 #pragma unroll
-    for (int i = 0; i < CH; ++i) load_row_chunk(p + 4 * i, r[i]);
+    for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
 }
 
-template <int G, int CH, int MINB, bool X>
+template <int G, int CH, int MINB, bool X, typename R>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                const double *__restrict__ rows, const LayerTermsDev *__restrict__ terms,
+                const R *__restrict__ rows, const LayerTermsT<R> *__restrict__ terms,
                 uint32_t n_layers)
 {
-    constexpr int W = 4 * G * CH;  // row width per layer (doubles)
-    constexpr int NCOL = 4 * CH;   // columns per lane
+    constexpr int PER = Chunk<R>::N;
+    constexpr int W = PER * G * CH;  // row width per layer (elements)
+    constexpr int NCOL = PER * CH;   // columns per lane
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;   // this lane's position in its group
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - c));
@@ -169,12 +198,12 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
     const uint32_t leader = lane - c;
-    const uint32_t row_stride = n_layers * W;  // doubles per union row
+    const uint32_t row_stride = n_layers * W;  // elements per union row
     const uint32_t C = s.catalogue_size;
 
-    double rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
-    double occ_ret = 0, occ_lim = 0, agg_ret = 0, agg_lim = 0;
-    const double *__restrict__ my_rows = rows;
+    R rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
+    R occ_ret = 0, occ_lim = 0, agg_ret = 0, agg_lim = 0;
+    const R *__restrict__ my_rows = rows;
     double *ylt_row = s.ylt;
     double *mo_row = nullptr, *inc_row = nullptr;  // F4 outputs (X only)
     uint32_t cur_layer = 0xffffffffu;
@@ -186,7 +215,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         if (t >= s.n_trials) break;
         const uint32_t layer = (uint32_t)(ticket - t * n_layers);
         if (layer != cur_layer) {
-            const LayerTermsDev &T = terms[layer];
+            const LayerTermsT<R> &T = terms[layer];
 #pragma unroll
             for (int j = 0; j < NCOL; ++j) {
                 rate[j] = T.rate[NCOL * c + j];
@@ -209,17 +238,17 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         const uint64_t k = s.offsets[t + 1] - base - beg;
         const uint32_t *ev = s.ids + beg;
         const uint32_t *const ev_end = ev + k;
-        double S = 0.0, Cprev = 0.0, lr = 0.0;  // lines 19, 25 (C_0 = 0), 28
-        double max_oc = 0.0, oc, inc;           // F4
+        R S = 0, Cprev = 0, lr = 0;  // lines 19, 25 (C_0 = 0), 28
+        R max_oc = 0, oc, inc;       // F4
         const bool writer = c == G - 1;
 
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
-            Row4 r[CH];
-            gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
-            event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
+            Chunk<R> r[CH];
+            gather<CH, R>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
+            event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
-            event_out<X>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
+            event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
         // body: chunks of 8 events.  Pipeline per group: the ids of chunk i+1 are in flight
@@ -232,8 +261,8 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             if (n_chunks > 1) load_ids8(ev + 8, id_n);
             uint32_t idx0 = map_index(map, id_c[0], C, bad);
             uint32_t idx1 = map_index(map, id_c[1], C, bad);
-            Row4 ra[CH];
-            gather<CH>(my_rows, row_stride, idx0, ra);
+            Chunk<R> ra[CH];
+            gather<CH, R>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
             for (uint64_t i = 0; i < n_chunks; ++i) {
                 const bool more = i + 1 < n_chunks;
@@ -244,16 +273,16 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                     const bool ok2 = j + 2 < 8 || more;
                     uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
-                    Row4 rb[CH];
-                    gather<CH>(my_rows, row_stride, pin(idx1, S), rb);
-                    event_step<G, CH>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
+                    Chunk<R> rb[CH];
+                    gather<CH, R>(my_rows, row_stride, pin(idx1, S), rb);
+                    event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
-                    event_out<X>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
+                    event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                     uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
-                    gather<CH>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
-                    event_step<G, CH>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
+                    gather<CH, R>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
+                    event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
-                    event_out<X>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1, writer);
+                    event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1, writer);
                     idx1 = idx3;
                 }
 #pragma unroll
@@ -264,16 +293,16 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         }
         // tail: remaining events one by one
         while (ev < ev_end) {
-            Row4 r[CH];
-            gather<CH>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
-            event_step<G, CH>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
+            Chunk<R> r[CH];
+            gather<CH, R>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
+            event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
-            event_out<X>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
+            event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
         if (writer) {
-            ylt_row[t] = lr;  // A8
-            if (X && mo_row) mo_row[t] = max_oc;
+            ylt_row[t] = (double)lr;  // A8
+            if (X && mo_row) mo_row[t] = (double)max_oc;
         }
         if (s.counter) {
             uint64_t next = 0;
@@ -317,14 +346,14 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
     if (e) atomicOr(err, e);
 }
 
-template <int G, int CH, int MINB = 1, bool X = false>
+template <int G, int CH, int MINB = 1, bool X = false, typename R = double>
 cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
 {
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, scan_kernel<G, CH, MINB, X>, kScanThreads, 0);
+            &occ, scan_kernel<G, CH, MINB, X, R>, kScanThreads, 0);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -347,8 +376,8 @@ cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
         blocks = (blocks + lcm - 1) / lcm * lcm;
     if (blocks > max_blocks) blocks = max_blocks;
-    scan_kernel<G, CH, MINB, X><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
-        s, st.d_map, st.d_rows, st.d_terms, st.n_layers);
+    scan_kernel<G, CH, MINB, X, R><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
+        s, st.d_map, (const R *)st.d_rows, (const LayerTermsT<R> *)st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
 
@@ -359,6 +388,20 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
+    if (st.bits == 32) {  // F3: fp32 store (widths in floats: 8, 16, 32, 64)
+        const bool x = s.max_occ || s.event_inc;
+        switch (st.width) {
+            case 8: return x ? launch_gc<1, 1, 1, true, float>(st, s, sm_count, stream)
+                             : launch_gc<1, 1, 1, false, float>(st, s, sm_count, stream);
+            case 16: return x ? launch_gc<2, 1, 1, true, float>(st, s, sm_count, stream)
+                              : launch_gc<2, 1, 1, false, float>(st, s, sm_count, stream);
+            case 32: return x ? launch_gc<2, 2, 1, true, float>(st, s, sm_count, stream)
+                              : launch_gc<2, 2, 1, false, float>(st, s, sm_count, stream);
+            case 64: return x ? launch_gc<4, 2, 1, true, float>(st, s, sm_count, stream)
+                              : launch_gc<4, 2, 1, false, float>(st, s, sm_count, stream);
+            default: --*launches; return cudaErrorInvalidValue;
+        }
+    }
     if (s.max_occ || s.event_inc) {  // F4 outputs: default decomposition only
         switch (st.width) {
             case 4: return launch_gc<1, 1, 1, true>(st, s, sm_count, stream);

@@ -407,3 +407,63 @@ def test_f4_outputs(stream, preset, kw):
         ctx.ara_run_outputs(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, mo,
                             inc, event_inc_ld=max(n_ev - 1, 1))
     ctx.close()
+
+
+# --------------------------------------------------------------------------- F3 (fp32)
+def make_ctx32(ds, stream):
+    ctx = ara.Context(0, stream)
+    ctx.ara_set_precision(32)
+    ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    return ctx
+
+
+@pytest.mark.parametrize("preset,kw", [("tiny", dict(seed=7)),
+                                       ("tiny", dict(n_elts=24, elts_per_layer=24, k_min=0,
+                                                     k_max=30, n_trials=500)),
+                                       ("tiny", dict(n_elts=64, elts_per_layer=64, n_trials=300)),
+                                       ("medium", dict(n_trials=2000)),
+                                       ("portfolio", dict(n_trials=400, k_min=50, k_max=200))])
+def test_f32_bit_identical_to_f32_oracle(stream, preset, kw):
+    """F3: the fp32 store and scan reproduce the float instantiation of the oracle bit for bit
+    (both round each input to float once and run Algorithm 1 in float in the same order)."""
+    ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
+    want = oracle.run_analysis(ds, n_threads=8, precision=32)
+    ctx = make_ctx32(ds, stream)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx), want)
+    y_o, mo_o, inc_o = oracle.run_analysis(ds, n_threads=8, precision=32, outputs=True)
+    L, n, n_ev = ds.n_layers, ds.n_trials, int(ds.trial_offsets[-1])
+    ylt = torch.empty((L, n), dtype=torch.float64, device=DEV)
+    mo = torch.empty((L, n), dtype=torch.float64, device=DEV)
+    inc = torch.empty((L, n_ev), dtype=torch.float64, device=DEV)
+    ctx.ara_run_outputs(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, mo, inc,
+                        flags=ara.ARA_RUN_SYNC)
+    assert_bit_identical(mo.cpu().numpy(), mo_o)
+    assert_bit_identical(inc.cpu().numpy(), inc_o)
+    m, rows = ctx.ara_export_store(0, ds.catalogue_size)
+    j = int(ds.elt_index[0])
+    a, b = int(ds.rec_offsets[j]), int(ds.rec_offsets[j + 1])
+    assert np.array_equal(rows[m[ds.rec_event_ids[a:b]], 0],
+                          ds.rec_losses[a:b].astype(np.float32).astype(np.float64))
+    ctx.close()
+
+
+def test_f32_error_distribution_vs_f64(stream):
+    """F3 against the fp64 path on the medium shape: report the distribution the north star asks
+    for (SPEC.md L283's 1e-4 relative bar fails where S - AggR cancels); assert the float
+    rounding bound and that switching precision back restores the bit-identical fp64 path."""
+    ds = datagen.generate(datagen.PRESETS["medium"].replace(n_trials=3000))
+    ctx = make_ctx32(ds, stream)
+    y32 = gpu_ylt(ds, stream, ctx=ctx)[0]
+    y64 = oracle.run_analysis(ds, n_threads=8)[0]
+    aggR, aggL = ds.layer_terms[0, 2:]
+    rel = np.abs(y32 - y64) / np.maximum(np.abs(y64), 1e-300)
+    frac_ok = float(np.mean((rel <= 1e-4) | (y64 == y32)))
+    print(f"fp32 vs fp64: {frac_ok:.4f} of YLT entries within 1e-4 relative; max abs "
+          f"{np.max(np.abs(y32 - y64)):.3e} (AggL {aggL:.3e})")
+    assert np.max(np.abs(y32 - y64)) <= 8 * (1000 + 16 + 2) * 2.0 ** -24 * (aggR + aggL) * 4
+    assert frac_ok > 0.5
+    ctx.ara_set_precision(64)
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx)[0:1], y64[None, :])
+    ctx.close()

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--variants", default="2:0,4:0,1:0")
     ap.add_argument("--flags", type=int, default=0, help="ara_run flags (4 = ARA_RUN_BALANCE)")
     ap.add_argument("--sched", default="", help="ARA_SCAN_SCHED: static | dynamic")
+    ap.add_argument("--precision", type=int, default=64)
     args = ap.parse_args()
     import torch
 
@@ -39,7 +40,7 @@ def main():
     E = spec.elts_per_layer
     n, n_ev = ds.n_trials, int(ds.trial_offsets[-1])
     L = ds.n_layers
-    bytes_alg = n_ev * (4 + 8 * E * L) + 8 * n * L + 8 * (n + 1)
+    bytes_alg = n_ev * (4 + args.precision // 8 * E * L) + 8 * n * L + 8 * (n + 1)
     ref = None
     for v in args.variants.split(","):
         g, mb = v.split(":")
@@ -47,6 +48,7 @@ def main():
         os.environ["ARA_SCAN_MINB"] = mb
         os.environ["ARA_SCAN_SCHED"] = args.sched
         ctx = ara.Context(0, stream)
+        ctx.ara_set_precision(args.precision)
         ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses,
                           ds.fin)
         ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
