@@ -81,9 +81,12 @@ typedef struct {
 #define ARA_RUN_VALIDATE 2u /* check offsets and event ids on the device BEFORE the scan
                                (one extra YET read); implies ARA_RUN_SYNC; on error nothing
                                is written to the YLT                                        */
-#define ARA_RUN_BALANCE 4u  /* hand trials to thread groups dynamically (one atomic ticket
-                               per trial and layer): use for variable-length trials (PAPER.md
-                               L43: 800-1500 events); results are identical either way      */
+#define ARA_RUN_BALANCE 4u  /* length-bucketed scheduling for variable-length trials
+                               (800-1500 events): the trials are sorted by
+                               length on the device and handed out in warp-sized batches, so
+                               the thread groups of a warp run trials of nearly equal length.
+                               This is the default schedule; the flag is accepted for clarity.
+                               Results are identical under any schedule.                     */
 
 /* Human-readable name of a status code (static storage). */
 const char *ara_status_string(ara_status s);

@@ -45,6 +45,7 @@ struct ara_ctx {
     uint32_t *h_err = nullptr;  // pinned mirror
     uint64_t launches = 0;
     ara::MetricsScratch metrics;
+    ara::SortScratch sort;
 
     // ara_run_host staging (double-buffered)
     uint32_t *d_ids_stage[2] = {nullptr, nullptr};
@@ -161,17 +162,25 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                          double *d_ylt, uint64_t ld, uint32_t flags,
                          const ara_outputs *extra = nullptr)
 {
-    // Dynamic ticket scheduling (one atomic per trial and layer) balances variable-length
-    // trials; it is the default for a single layer.  With several layers the static
-    // assignment keeps the groups of one trial side by side (shared id and map requests)
-    // unless ARA_RUN_BALANCE asks for dynamic tickets.  Results are identical either way.
-    const bool dyn = ctx->sched == 2 ||
-                     (ctx->sched == 0 && ((flags & ARA_RUN_BALANCE) || ctx->store.n_layers == 1));
+    // Scheduling (results are identical either way).  Default: trials sorted by length on the
+    // device and handed out in warp-sized batches, so the thread groups of a warp run trials of
+    // nearly equal length (variable-length YETs keep full SIMT width; measured neutral for
+    // equal lengths, profiles/README.md).  ARA_SCAN_SCHED=static|dynamic selects the plain
+    // round-robin / per-group ticket schedules (tuning); the F4 outputs use per-group tickets.
+    const bool balance = ctx->sched == 0 && !extra;
+    const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
+    const uint32_t *perm = nullptr;
+    if (balance) {
+        cudaError_t e = ara::launch_length_sort(d_off, n, ctx->sort, ctx->sm_count, ctx->stream,
+                                                &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "length sort");
+        perm = ctx->sort.perm;
+    }
     ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
                       dyn ? ctx->d_ticket : nullptr,
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
-                      extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0};
+                      extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm};
     cudaError_t e = ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
@@ -301,6 +310,7 @@ void ara_destroy(ara_ctx *ctx)
     cudaFree(ctx->d_ticket);
     cudaFreeHost(ctx->h_err);
     cudaFree(ctx->metrics.d_buf);
+    cudaFree(ctx->sort.d_buf);
     for (int i = 0; i < 2; ++i) {
         cudaFree(ctx->d_ids_stage[i]);
         cudaFree(ctx->d_off_stage[i]);

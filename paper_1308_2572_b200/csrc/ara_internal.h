@@ -95,7 +95,17 @@ struct ScanLaunch {
     uint64_t max_occ_ld;
     double *event_inc;            // F4: [n_layers][event_inc_ld] or NULL (YET positions)
     uint64_t event_inc_ld;
+    const uint32_t *perm;         // length-sorted trial order (ARA_RUN_BALANCE) or NULL
 };
+
+// Scratch of the length sort (ARA_RUN_BALANCE): keys, indices, CUB temporary storage.
+struct SortScratch {
+    void *d_buf = nullptr;
+    size_t bytes = 0;
+    const uint32_t *perm = nullptr;  // result of the last sort (inside d_buf)
+};
+cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch &sc, int sm_count,
+                               cudaStream_t stream, uint64_t *launches);
 
 // scan.cu
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,

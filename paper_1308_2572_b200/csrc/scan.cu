@@ -24,6 +24,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "ara_internal.h"
 
 namespace ara {
@@ -177,7 +179,7 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
     for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
 }
 
-template <int G, int CH, int MINB, bool X, typename R>
+template <int G, int CH, int MINB, bool X, typename R, bool BAL>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                 const R *__restrict__ rows, const LayerTermsT<R> *__restrict__ terms,
@@ -208,12 +210,23 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     double *mo_row = nullptr, *inc_row = nullptr;  // F4 outputs (X only)
     uint32_t cur_layer = 0xffffffffu;
 
+    // Length-bucketed mode (s.perm, ARA_RUN_BALANCE): tickets index trials in the order of
+    // s.perm (sorted by length) and are taken a warp-sized batch at a time, so the groups of a
+    // warp run trials of nearly equal length and stay converged.
+    constexpr bool batched = BAL;  // s.perm != nullptr
+    const uint32_t B = 32 / G, gw = lane / G;  // groups per warp, this group's index in it
+    const uint64_t warp_g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) / 32;
+    const uint64_t n_tickets = s.n_trials * n_layers;
+
     const uint64_t base = s.offsets[0];
     bool bad = false;
-    for (uint64_t ticket = g;;) {
-        const uint64_t t = ticket / n_layers;
-        if (t >= s.n_trials) break;
-        const uint32_t layer = (uint32_t)(ticket - t * n_layers);
+    for (uint64_t ticket = batched ? warp_g * B + gw : g;;) {
+        if (batched ? ticket - gw >= n_tickets : ticket >= n_tickets) break;  // warp-uniform
+        if (ticket < n_tickets) {
+        const uint64_t q = ticket / n_layers;
+        const uint64_t t = batched ? (uint64_t)s.perm[q] : q;
+        const uint32_t layer = (uint32_t)(ticket - q * n_layers);
         if (layer != cur_layer) {
             const LayerTermsT<R> &T = terms[layer];
 #pragma unroll
@@ -304,7 +317,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             ylt_row[t] = (double)lr;  // A8
             if (X && mo_row) mo_row[t] = (double)max_oc;
         }
-        if (s.counter) {
+        }  // ticket < n_tickets
+        if (batched) {
+            __syncwarp();
+            uint64_t b = 0;
+            if (lane == 0) b = warps + atomicAdd(s.counter, 1ull);
+            ticket = __shfl_sync(0xffffffffu, b, 0) * B + gw;
+        } else if (s.counter) {
             uint64_t next = 0;
             if (c == 0) next = groups + atomicAdd(s.counter, 1ull);
             ticket = __shfl_sync(gmask, next, leader);
@@ -346,14 +365,26 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
     if (e) atomicOr(err, e);
 }
 
-template <int G, int CH, int MINB = 1, bool X = false, typename R = double>
+// Keys for the length sort: trial lengths (saturated to 32 bits) and trial indices.
+__global__ void length_keys_kernel(const uint64_t *__restrict__ offsets, uint64_t n,
+                                   uint32_t *keys, uint32_t *idx)
+{
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t len = offsets[t + 1] - offsets[t];
+        keys[t] = len > 0xffffffffull ? 0xffffffffu : (uint32_t)len;
+        idx[t] = (uint32_t)t;
+    }
+}
+
+template <int G, int CH, int MINB = 1, bool X = false, typename R = double, bool BAL = false>
 cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
 {
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, scan_kernel<G, CH, MINB, X, R>, kScanThreads, 0);
+            &occ, scan_kernel<G, CH, MINB, X, R, BAL>, kScanThreads, 0);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -376,7 +407,7 @@ cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
         blocks = (blocks + lcm - 1) / lcm * lcm;
     if (blocks > max_blocks) blocks = max_blocks;
-    scan_kernel<G, CH, MINB, X, R><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
+    scan_kernel<G, CH, MINB, X, R, BAL><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
         s, st.d_map, (const R *)st.d_rows, (const LayerTermsT<R> *)st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
@@ -388,6 +419,26 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
+    if (s.perm && !(s.max_occ || s.event_inc)) {  // length-bucketed (ARA_RUN_BALANCE)
+        if (st.bits == 32) {
+            switch (st.width) {
+                case 8: return launch_gc<1, 1, 1, false, float, true>(st, s, sm_count, stream);
+                case 16: return launch_gc<2, 1, 1, false, float, true>(st, s, sm_count, stream);
+                case 32: return launch_gc<2, 2, 1, false, float, true>(st, s, sm_count, stream);
+                case 64: return launch_gc<4, 2, 1, false, float, true>(st, s, sm_count, stream);
+                default: --*launches; return cudaErrorInvalidValue;
+            }
+        }
+        switch (st.width) {
+            case 4: return launch_gc<1, 1, 1, false, double, true>(st, s, sm_count, stream);
+            case 8: return launch_gc<2, 1, 1, false, double, true>(st, s, sm_count, stream);
+            case 16: return launch_gc<2, 2, 3, false, double, true>(st, s, sm_count, stream);
+            case 32: return launch_gc<4, 2, 1, false, double, true>(st, s, sm_count, stream);
+            case 48: return launch_gc<4, 3, 1, false, double, true>(st, s, sm_count, stream);
+            case 64: return launch_gc<4, 4, 1, false, double, true>(st, s, sm_count, stream);
+            default: --*launches; return cudaErrorInvalidValue;
+        }
+    }
     if (st.bits == 32) {  // F3: fp32 store (widths in floats: 8, 16, 32, 64)
         const bool x = s.max_occ || s.event_inc;
         switch (st.width) {
@@ -434,6 +485,39 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
         case 1 * 16 + 4: return launch_gc<1, 4>(st, s, sm_count, stream);  // W = 16, G = 1
         default: --*launches; return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch &sc, int sm_count,
+                               cudaStream_t stream, uint64_t *launches)
+{
+    if (n == 0) return cudaSuccess;
+    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
+        nullptr, temp, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const uint32_t *)nullptr,
+        (uint32_t *)nullptr, (int)n, 0, 32, stream);
+    if (e != cudaSuccess) return e;
+    const size_t need = 4 * (size_t)n * 4 + temp + 256;
+    if (sc.bytes < need) {
+        cudaFree(sc.d_buf);
+        sc.d_buf = nullptr;
+        sc.bytes = 0;
+        e = cudaMalloc(&sc.d_buf, need);
+        if (e != cudaSuccess) return e;
+        sc.bytes = need;
+    }
+    uint32_t *keys_in = (uint32_t *)sc.d_buf, *keys_out = keys_in + n;
+    uint32_t *idx_in = keys_out + n, *idx_out = idx_in + n;
+    void *tmp = (void *)(((uintptr_t)(idx_out + n) + 255) & ~(uintptr_t)255);
+    ++*launches;
+    length_keys_kernel<<<sm_count * 4, 256, 0, stream>>>(offsets, n, keys_in, idx_in);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++*launches;  // the CUB radix sort (a few internal kernels)
+    e = cub::DeviceRadixSort::SortPairsDescending(tmp, temp, keys_in, keys_out, idx_in, idx_out,
+                                                  (int)n, 0, 32, stream);
+    sc.perm = idx_out;
+    return e;
 }
 
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
