@@ -217,10 +217,18 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using {world}")
+    # Test hook: ARA_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 over gloo (NCCL refuses two
+    # ranks on one GPU), so the multi-rank path can be exercised on a 1-GPU box.
+    same_dev = os.environ.get("ARA_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     # ---- inputs: ELTs/layers are identical on every rank (seeded); each rank generates only
     # its own trial slice of the YET (counter-based substreams), so the YET is never sent.
@@ -293,9 +301,7 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in scan_ev)
     if world > 1:
-        t = torch.tensor([ms, scan_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, scan_ms = t.tolist()
+        ms, scan_ms = adist.max_over_ranks([ms, scan_ms])
 
     trial_events = spec.trial_events * spec.n_layers
     value = trial_events / (ms * 1e-3)
@@ -340,9 +346,7 @@ def main():
             ts.append(time.perf_counter() - tt)
         t_e2e = statistics.median(ts)
         if world > 1:
-            t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t_e2e = t.item()
+            t_e2e = adist.max_over_ranks([t_e2e])[0]
         h2d = (n_loc + 1) * 8 + n_ev * 4 + L * n_loc * 8
         d2h = L * n_loc * 8 + L * len(P) * 16
         e2e = {"value": trial_events / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,

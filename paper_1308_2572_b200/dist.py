@@ -41,6 +41,10 @@ def _dev_for(dist, like=None):
     return torch.device("cpu")
 
 
+def _host_staged(dist) -> bool:
+    return dist.get_backend() != "nccl"
+
+
 def broadcast_inputs(ds, src: int = 0):
     """Broadcast the raw ELT records, terms and layer membership of ``ds`` from ``src`` to every
     rank (in place on the non-source ranks' arrays, which must have the same shapes; use
@@ -77,6 +81,10 @@ def gather_ylt(ylt_local, n_trials: int, out=None):
     m = max(b - a for a, b in parts)
     equal = all(b - a == m for a, b in parts)
     nccl = dist.get_backend() == "nccl"
+    if not nccl and ylt_local.is_cuda:  # gloo: stage through host memory
+        host = gather_ylt(ylt_local.cpu(), n_trials)
+        out.copy_(host)
+        return out
     for l in range(L):
         row = ylt_local[l].contiguous()
         if equal and nccl:
