@@ -31,7 +31,7 @@ struct MetricsParams {
     uint32_t *hist;                // [kPasses][ARA_MAX_P][kBins]
     double *part_sum;              // [grid][ARA_MAX_P]
     unsigned long long *part_cnt;  // [grid][ARA_MAX_P]
-    double *out;                   // [2][ARA_MAX_P]: pml, tvar
+    double *out;                   // [2][n_p]: pml, tvar
 };
 
 // Order-preserving map of finite doubles to u64 (-0 canonicalised to +0).
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
         }
         const double q = from_key(s_prefix[i]);
         P.out[i] = q;
-        P.out[ARA_MAX_P + i] = q + s / (double)c;
+        P.out[n_p + i] = q + s / (double)c;
     }
 }
 
@@ -204,13 +204,13 @@ cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const 
     e = cudaLaunchCooperativeKernel((void *)metrics_kernel, grid, kThreads, args, 0, stream);
     if (e != cudaSuccess) return e;
     double host[2 * ARA_MAX_P];
-    e = cudaMemcpyAsync(host, P.out, sizeof(host), cudaMemcpyDeviceToHost, stream);
+    e = cudaMemcpyAsync(host, P.out, 2 * n_p * sizeof(double), cudaMemcpyDeviceToHost, stream);
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return e;
     for (uint32_t i = 0; i < n_p; ++i) {
         pml_out[i] = host[i];
-        tvar_out[i] = host[ARA_MAX_P + i];
+        tvar_out[i] = host[n_p + i];
     }
     return cudaSuccess;
 }
