@@ -52,12 +52,19 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
 {
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t sh[ARA_MAX_P][kBins];
-    __shared__ uint64_t s_prefix[ARA_MAX_P];
-    __shared__ uint64_t s_rank[ARA_MAX_P];
+    __shared__ uint64_t s_prefix[ARA_MAX_P];  // per probability: key prefix found so far
+    __shared__ uint64_t s_rank[ARA_MAX_P];    // per probability: rank within that prefix
+    __shared__ uint64_t s_uprefix[ARA_MAX_P]; // distinct prefixes of this pass
+    __shared__ uint32_t s_uof[ARA_MAX_P];     // probability -> its distinct prefix
+    __shared__ uint32_t s_nu;
+    __shared__ uint64_t s_wsum[kThreads / 32];
+    __shared__ uint64_t s_prefix_n[ARA_MAX_P];
+    __shared__ uint64_t s_rank_n[ARA_MAX_P];
     __shared__ double s_red[kThreads / 32];
     __shared__ unsigned long long s_redc[kThreads / 32];
 
     const uint32_t n_p = P.n_p;
+    const uint32_t lane = threadIdx.x & 31u;
     const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
 
@@ -71,46 +78,95 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
     for (int pass = 0; pass < kPasses; ++pass) {
         const int shift = 56 - 8 * pass;
         const uint64_t mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+        // Probabilities whose prefixes agree share one histogram (early passes: all of them),
+        // and two distinct prefixes of the same length are disjoint, so every element adds to
+        // at most one histogram.
+        if (threadIdx.x == 0) {
+            uint32_t nu = 0;
+            for (uint32_t i = 0; i < n_p; ++i) {
+                uint32_t u = 0;
+                while (u < nu && s_uprefix[u] != (s_prefix[i] & mask)) ++u;
+                if (u == nu) s_uprefix[nu++] = s_prefix[i] & mask;
+                s_uof[i] = u;
+            }
+            s_nu = nu;
+        }
         for (uint32_t i = threadIdx.x; i < n_p * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
         __syncthreads();
-        for (uint64_t e = gtid; e < P.n; e += gstride) {
-            const uint64_t key = to_key(P.v[e]);
-            for (uint32_t i = 0; i < n_p; ++i)
-                if ((key & mask) == (s_prefix[i] & mask))
-                    atomicAdd(&sh[i][(key >> shift) & 0xff], 1u);
+        const uint32_t nu = s_nu;
+        for (uint64_t e0 = gtid - lane; e0 < P.n; e0 += gstride) {  // warp-uniform trip count
+            const uint64_t e = e0 + lane;
+            uint32_t slot = 0xffffffffu;  // (distinct prefix, digit) or none
+            if (e < P.n) {
+                const uint64_t key = to_key(P.v[e]);
+                for (uint32_t u = 0; u < nu; ++u)
+                    if ((key & mask) == s_uprefix[u]) slot = u * kBins + ((key >> shift) & 0xff);
+            }
+            // warp-aggregated histogram update: one atomic per distinct slot in the warp
+            const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+            if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(&sh[0][0] + slot, (uint32_t)__popc(peers));
         }
         __syncthreads();
         uint32_t *gh = P.hist + (size_t)pass * ARA_MAX_P * kBins;
-        for (uint32_t i = threadIdx.x; i < n_p * kBins; i += blockDim.x) {
+        for (uint32_t i = threadIdx.x; i < nu * kBins; i += blockDim.x) {
             const uint32_t c = (&sh[0][0])[i];
             if (c) atomicAdd(gh + i, c);
         }
         grid.sync();
-        if (threadIdx.x < n_p) {  // every block walks the same global histogram
-            const uint32_t i = threadIdx.x;
-            uint64_t r = s_rank[i], cum = 0;
-            for (int b = 0; b < kBins; ++b) {
-                const uint64_t c = __ldcg(gh + (size_t)i * kBins + b);
-                if (r < cum + c) {
-                    s_prefix[i] |= (uint64_t)b << shift;
-                    s_rank[i] = r - cum;
-                    break;
-                }
-                cum += c;
+        // Every block reads the merged histograms (one bin per thread), scans them, and each
+        // probability finds the bin holding its rank: no serial walk over dependent L2 loads.
+        static_assert(kThreads == kBins, "one bin per thread");
+        for (uint32_t u = 0; u < nu; ++u) {
+            const uint64_t cnt = __ldcg(gh + (size_t)u * kBins + threadIdx.x);
+            uint64_t incl = cnt;  // inclusive prefix sum over the 256 bins
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
             }
+            if (lane == 31) s_wsum[threadIdx.x >> 5] = incl;
+            __syncthreads();
+            uint64_t before = 0;
+            for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) before += s_wsum[w];
+            incl += before;
+            const uint64_t excl = incl - cnt;
+            for (uint32_t i = 0; i < n_p; ++i) {
+                const uint64_t r = s_rank[i];
+                if (s_uof[i] == u && r >= excl && r < incl) {
+                    s_prefix_n[i] = s_prefix[i] | ((uint64_t)threadIdx.x << shift);
+                    s_rank_n[i] = r - excl;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < n_p) {
+            s_prefix[threadIdx.x] = s_prefix_n[threadIdx.x];
+            s_rank[threadIdx.x] = s_rank_n[threadIdx.x];
         }
         __syncthreads();
     }
 
-    // Tail sums over this block's contiguous chunk, per probability, in a fixed order.  The sum
-    // is of (v - PML) >= 0, so TVaR = PML + mean(v - PML) >= PML holds exactly and the
-    // rounding error scales with the tail's spread, not its level.
+    // Tail sums over this block's contiguous chunk in a fixed order, once per distinct PML (equal
+    // order statistics have equal tails).  The sum is of (v - PML) >= 0, so TVaR = PML +
+    // mean(v - PML) >= PML holds exactly and the rounding error scales with the tail's spread.
+    if (threadIdx.x == 0) {
+        uint32_t nu = 0;
+        for (uint32_t i = 0; i < n_p; ++i) {
+            uint32_t u = 0;
+            while (u < nu && s_uprefix[u] != s_prefix[i]) ++u;
+            if (u == nu) s_uprefix[nu++] = s_prefix[i];
+            s_uof[i] = u;
+        }
+        s_nu = nu;
+    }
+    __syncthreads();
+    const uint32_t nu = s_nu;
     const uint64_t chunk = (P.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < P.n ? lo + chunk : P.n;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t i = 0; i < n_p; ++i) {
-        const uint64_t q = s_prefix[i];
+    const int warp = threadIdx.x >> 5;
+    for (uint32_t u = 0; u < nu; ++u) {
+        const uint64_t q = s_uprefix[u];
         const double qv = from_key(q);
         double s = 0.0;
         unsigned long long c = 0;
@@ -137,19 +193,19 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
                 bs += s_red[w];
                 bc += s_redc[w];
             }
-            P.part_sum[(size_t)blockIdx.x * ARA_MAX_P + i] = bs;
-            P.part_cnt[(size_t)blockIdx.x * ARA_MAX_P + i] = bc;
+            P.part_sum[(size_t)blockIdx.x * ARA_MAX_P + u] = bs;
+            P.part_cnt[(size_t)blockIdx.x * ARA_MAX_P + u] = bc;
         }
         __syncthreads();
     }
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x < n_p) {
-        const uint32_t i = threadIdx.x;
+        const uint32_t i = threadIdx.x, u = s_uof[i];
         double s = 0.0;
         unsigned long long c = 0;
         for (uint32_t b = 0; b < gridDim.x; ++b) {
-            s += __ldcg(P.part_sum + (size_t)b * ARA_MAX_P + i);
-            c += __ldcg(P.part_cnt + (size_t)b * ARA_MAX_P + i);
+            s += __ldcg(P.part_sum + (size_t)b * ARA_MAX_P + u);
+            c += __ldcg(P.part_cnt + (size_t)b * ARA_MAX_P + u);
         }
         const double q = from_key(s_prefix[i]);
         P.out[i] = q;
