@@ -28,6 +28,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-fno-fast-m
 # explicitly); the oracle's reading R7 fixes separately rounded products and differences.
 PER_FILE = {
     "scan.cu": ["-fmad=false", "-Xptxas", "-v"],
+    "portfolio.cu": ["-fmad=false", "-Xptxas", "-v"],
     "metrics.cu": ["-Xptxas", "-v"],
     "ara.cpp": [],
 }
@@ -41,7 +42,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = _sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "ara.h"),
+    deps = _sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(
+        os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "ara.h"),
                                                                  os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps)
 

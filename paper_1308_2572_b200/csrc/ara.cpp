@@ -109,6 +109,8 @@ void free_layers(ara_ctx *ctx)
     cudaFree(ctx->store.d_map);
     cudaFree(ctx->store.d_rows);
     cudaFree(ctx->store.d_terms);
+    cudaFree(ctx->store.uni.d_rows);
+    cudaFree(ctx->store.uni.d_terms);
     ctx->store = ara::DeviceStore();
     ctx->store_bytes = 0;
     ctx->have_layers = false;
@@ -181,7 +183,11 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
                       extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm};
-    cudaError_t e = ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
+    cudaError_t e =
+        (ctx->store.uni.enabled && !extra)
+            ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, s, ctx->sm_count,
+                                    ctx->stream, &ctx->launches)
+            : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
 }
@@ -221,6 +227,76 @@ void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vecto
         lt[l].agg_ret = (R)terms[l].agg_retention;
         lt[l].agg_lim = (R)terms[l].agg_limit;
     }
+}
+
+// F1 union-row store (portfolio.cu) when the portfolio qualifies; returns ARA_OK either way
+// unless a CUDA call fails.
+ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
+                       const ara_layer_terms *terms, const uint32_t *elt_offsets,
+                       const uint32_t *elt_index)
+{
+    ara::DeviceStore &st = ctx->store;
+    const uint32_t L = st.n_layers;
+    if (ctx->bits != 64 || L < 2 || L > (uint32_t)ara::kUnionMaxLayers) return ARA_OK;
+    if (const char *e = getenv("ARA_PORTFOLIO"))
+        if (atoi(e) == 0) return ARA_OK;
+    std::vector<uint32_t> J;  // distinct ELTs in order of first appearance
+    std::vector<int> col_of(ctx->n_elts, -1);
+    for (uint32_t l = 0; l < L; ++l) {
+        if (st.n_cols[l] > (uint32_t)ara::kUnionMaxE) return ARA_OK;
+        for (uint32_t c = elt_offsets[l]; c < elt_offsets[l + 1]; ++c)
+            if (col_of[elt_index[c]] < 0) {
+                col_of[elt_index[c]] = (int)J.size();
+                J.push_back(elt_index[c]);
+            }
+    }
+    if (J.size() > (size_t)ara::kMaxCols) return ARA_OK;
+    uint32_t GU = 2;
+    while (8 * GU < J.size() || GU < L) GU *= 2;
+    if (GU > 8) return ARA_OK;
+    const uint32_t WU = 8 * GU;
+    auto u_slot = [](uint32_t col) { return col + 2 * (col >> 3); };
+    std::vector<double> rows((size_t)(st.n_union + 1) * WU, 0.0);
+    ara::UnionTermsDev ut{};
+    for (uint32_t col = 0; col < WU; ++col) {  // padding columns: neutral terms, zero losses
+        ut.rate[col] = 1.0;
+        ut.ret[col] = 0.0;
+        ut.lim[col] = INFINITY;
+    }
+    for (uint32_t col = 0; col < J.size(); ++col) {
+        const uint32_t j = J[col];
+        for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)  // bit copies
+            rows[(size_t)map[ctx->rec_ids[r]] * WU + col] = ctx->rec_losses[r];
+        ut.rate[col] = ctx->fin[j].rate;
+        ut.ret[col] = ctx->fin[j].retention;
+        ut.lim[col] = ctx->fin[j].limit;
+    }
+    ut.n_layers = L;
+    for (uint32_t l = 0; l < (uint32_t)ara::kUnionMaxLayers; ++l) {
+        const bool real = l < L;
+        ut.occ_ret[l] = real ? terms[l].occ_retention : 0.0;
+        ut.occ_lim[l] = real ? terms[l].occ_limit : 0.0;
+        ut.agg_ret[l] = real ? terms[l].agg_retention : 0.0;
+        ut.agg_lim[l] = real ? terms[l].agg_limit : 0.0;
+        for (uint32_t i = 0; i < (uint32_t)ara::kUnionMaxE; ++i) {
+            // layer order = summation order; past the layer's ELTs: the zero slot (+0 neutral)
+            uint32_t slot = u_slot(WU);
+            if (real && i < st.n_cols[l]) slot = u_slot(col_of[elt_index[elt_offsets[l] + i]]);
+            ut.slot2[l][i / 2] |= slot << (16 * (i % 2));
+        }
+    }
+    ara::UnionStore &us = st.uni;
+    us.GU = GU;
+    us.n_cols = (uint32_t)J.size();
+    const size_t row_bytes = rows.size() * 8;
+    cudaError_t e = cudaMalloc(&us.d_rows, row_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&us.d_terms, sizeof(ut));
+    if (e == cudaSuccess) e = cudaMemcpy(us.d_rows, rows.data(), row_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(us.d_terms, &ut, sizeof(ut), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "union store");
+    us.enabled = true;
+    ctx->store_bytes += row_bytes + sizeof(ut);
+    return ARA_OK;
 }
 
 }  // namespace
@@ -473,6 +549,11 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
             return cuda_fail(ctx, e, "device ELT store");
         }
         ctx->store_bytes = map_bytes + row_bytes + term_bytes;
+        ara_status us = build_union(ctx, map, terms, elt_offsets, elt_index);
+        if (us != ARA_OK) {
+            free_layers(ctx);
+            return us;
+        }
         ctx->have_layers = true;
         return ARA_OK;
     });

@@ -65,6 +65,27 @@ inline ScanShape scan_shape_for_width(uint32_t W, int override_g)
     return {4, (int)(W / 16)};
 }
 
+// Union-row store for multi-layer portfolios (F1, portfolio.cu): the distinct ELTs J of all
+// layers (|J| <= 64) are the columns of one row per event; each layer lists its columns in its
+// own summation order.  Used when 2 <= n_layers <= 8, every layer has <= 16 ELTs and the store is
+// fp64; otherwise the per-layer rows below serve the scan.
+constexpr int kUnionMaxLayers = 8;
+constexpr int kUnionMaxE = 16;
+struct UnionTermsDev {
+    double rate[kMaxCols], ret[kMaxCols], lim[kMaxCols];  // per union column (padding neutral)
+    double occ_ret[kUnionMaxLayers], occ_lim[kUnionMaxLayers];
+    double agg_ret[kUnionMaxLayers], agg_lim[kUnionMaxLayers];
+    uint32_t slot2[kUnionMaxLayers][kUnionMaxE / 2];  // packed 16-bit shared-memory F slots
+    uint32_t n_layers;
+};
+struct UnionStore {
+    bool enabled = false;
+    uint32_t GU = 0;         // lanes per trial (2, 4 or 8); union row width WU = 8 * GU doubles
+    uint32_t n_cols = 0;     // |J|
+    double *d_rows = nullptr;            // [(U+1) * WU]
+    UnionTermsDev *d_terms = nullptr;
+};
+
 // Device ELT store of all layers: one catalogue map shared by the
 // layers and event-major rows that hold every layer's columns back to back, so one id read and
 // one map lookup per event serve all layers (F1, the layer-fused portfolio pass).
@@ -79,6 +100,7 @@ struct DeviceStore {
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     void *d_rows = nullptr;      // [(U+1) * n_layers * W] double or float, row 0 zero
     void *d_terms = nullptr;     // [n_layers] LayerTermsT<double or float>
+    UnionStore uni;              // F1 union rows (when eligible)
 };
 
 struct ScanLaunch {
@@ -110,6 +132,8 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
 // scan.cu
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
+                             int sm_count, cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
                             uint32_t catalogue_size, uint32_t *err, int sm_count,
                             cudaStream_t stream, uint64_t *launches);

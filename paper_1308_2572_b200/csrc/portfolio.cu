@@ -1,0 +1,252 @@
+// portfolio.cu -- layer-fused union-row scan for multi-layer portfolios (
+// Algorithm 1 line 2).
+//
+// The ELTs of all layers form one union set J (|J| <= 64).  Per event the kernel reads the id once,
+// looks up the shared catalogue map once, gathers ONE union row (the event's losses in every ELT
+// of J, 8|J| bytes), applies each ELT's financial terms ONCE (they are per ELT, reading R1), and
+// then every layer sums its own columns in its own listed order (lines 11-13), applies its own
+// occurrence and aggregate terms (lines 15-29) and writes its YLT entry.  Compared with per-layer
+// rows this halves the gathered bytes and the financial-term work when every ELT is shared by two
+// layers (configuration P).
+//
+// Decomposition: a group of GU lanes per trial (GU = 8 for 64 union columns).  Lane c owns the
+// 32-byte chunks c and c + GU of the union row (columns 4c..4c+3 and 4(c+GU)..4(c+GU)+3) and their
+// financial terms; the two gather instructions of a group each cover 32*GU contiguous bytes.  The
+// lanes write their F values to a per-group shared-memory row; after a warp-level barrier lane l
+// sums layer l's columns in layer order, ((0 + F_{c_l0}) + F_{c_l1}) + ..., exactly the oracle's
+// sequence, and carries layer l's running state.  Padding entries of a layer's column list point
+// at a zero slot (+0 is exactly neutral, reading R12).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ara_internal.h"
+#include "scan_common.cuh"
+
+namespace ara {
+namespace {
+using namespace scan_detail;
+
+// Shared-memory F row of one group: 8 doubles per 8 union columns plus 2 padding doubles, then a
+// zero pair; the group stride is odd (1 mod 16 doubles) so that the 32 lanes' 8-byte reads of
+// configuration P's layer columns hit every bank pair exactly twice (2 wavefronts, the minimum).
+__host__ __device__ constexpr int u_slot(int col) { return col + 2 * (col >> 3); }
+template <int GU>
+__host__ __device__ constexpr int u_row_doubles()
+{
+    return (u_slot(8 * GU) + 2 + 15) / 16 * 16 + 1;
+}
+
+template <int GU, bool BAL>
+__global__ void __launch_bounds__(kScanThreads, 3)
+    portfolio_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
+                     const double *__restrict__ urows, const UnionTermsDev *__restrict__ ut)
+{
+    constexpr int WU = 8 * GU;              // union row width (doubles)
+    constexpr int GS = u_row_doubles<GU>(); // shared F row stride per group (doubles)
+    constexpr int ZERO = u_slot(WU);        // index of the zero pair
+    __shared__ double sF[(kScanThreads / GU) * GS];
+
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t c = lane % GU;
+    const uint32_t gmask = (GU == 32) ? 0xffffffffu : (((1u << GU) - 1u) << (lane - c));
+    const uint32_t gb = threadIdx.x / GU;   // group index in the block
+    double *const myF = sF + gb * GS;
+    if (c == 0) {
+        myF[ZERO] = 0.0;
+        myF[ZERO + 1] = 0.0;
+    }
+
+    // financial terms of this lane's 8 union columns
+    double rate[8], ret[8], lim[8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * (c + GU * h) + q;
+            rate[4 * h + q] = ut->rate[col];
+            ret[4 * h + q] = ut->ret[col];
+            lim[4 * h + q] = ut->lim[col];
+        }
+    // this lane's layer (lane c -> layer c): terms and the shared-memory slots of its columns
+    const uint32_t n_layers = ut->n_layers;
+    const bool has_layer = c < n_layers;
+    const uint32_t ly = has_layer ? c : 0;
+    const double occ_ret = ut->occ_ret[ly], occ_lim = ut->occ_lim[ly];
+    const double agg_ret = ut->agg_ret[ly], agg_lim = ut->agg_lim[ly];
+    uint32_t slot2[kUnionMaxE / 2];  // two 16-bit slots per register
+#pragma unroll
+    for (int i = 0; i < kUnionMaxE / 2; ++i) slot2[i] = ut->slot2[ly][i];
+    double *const ylt_row = s.ylt + (size_t)ly * s.ylt_ld;
+    const double *__restrict__ my_rows = urows + 4 * c;
+    const uint32_t C = s.catalogue_size;
+    __syncwarp();
+
+    // one event: F of this lane's columns -> shared row -> this lane's layer sum and state
+    auto event = [&](const Chunk<double> (&r)[2], double &S, double &Cprev, double &lr) {
+        double f[8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int j = 4 * h + q;
+                const double l = rsub(rmul(r[h].v[q], rate[j]), ret[j]);  // line 9
+                f[j] = dmin(dmax0(l), lim[j]);
+            }
+        __syncwarp(gmask);  // the previous event's reads of the shared row are done
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double *dst = myF + u_slot(4 * (c + GU * h));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = f[4 * h + q];
+        }
+        __syncwarp(gmask);
+        double lo = 0.0;  // lines 11-13 for this lane's layer, in the layer's ELT order
+#pragma unroll
+        for (int i = 0; i < kUnionMaxE; ++i) {
+            const uint32_t sl = (slot2[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+            lo = radd(lo, myF[sl]);
+        }
+        const double oc = dmin(dmax0(rsub(lo, occ_ret)), occ_lim);  // line 16
+        S = radd(S, oc);                                              // line 19
+        const double Cd = dmin(dmax0(rsub(S, agg_ret)), agg_lim);     // line 22
+        lr = radd(lr, rsub(Cd, Cprev));                               // lines 25, 28
+        Cprev = Cd;
+    };
+    auto gather = [&](uint32_t idx, Chunk<double> (&r)[2]) {
+        const double *p = my_rows + (size_t)idx * WU;
+        load_row_chunk(p, r[0]);
+        load_row_chunk(p + 4 * GU, r[1]);
+    };
+
+    constexpr uint32_t B = 32 / GU;  // groups per warp
+    const uint32_t gw = lane / GU;
+    const uint64_t g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / GU;
+    const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / GU;
+    const uint64_t warp_g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) / 32;
+    const uint64_t base = s.offsets[0];
+    bool bad = false;
+    for (uint64_t ticket = BAL ? warp_g * B + gw : g;;) {
+        if (BAL ? ticket - gw >= s.n_trials : ticket >= s.n_trials) break;  // warp-uniform
+        if (ticket < s.n_trials) {
+            const uint64_t t = BAL ? (uint64_t)s.perm[ticket] : ticket;
+            const uint64_t beg = s.offsets[t] - base;
+            const uint64_t k = s.offsets[t + 1] - base - beg;
+            const uint32_t *ev = s.ids + beg;
+            const uint32_t *const ev_end = ev + k;
+            double S = 0.0, Cprev = 0.0, lr = 0.0;
+            while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {  // unaligned head
+                Chunk<double> r[2];
+                gather(map_index(map, load_id(ev), C, bad), r);
+                event(r, S, Cprev, lr);
+                ++ev;
+            }
+            const uint64_t n_chunks = (uint64_t)(ev_end - ev) / 8;
+            if (n_chunks) {
+                uint32_t id_c[8], id_n[8];
+                load_ids8(ev, id_c);
+                if (n_chunks > 1) load_ids8(ev + 8, id_n);
+                uint32_t idx1 = map_index(map, id_c[1], C, bad);
+                Chunk<double> ra[2];
+                gather(map_index(map, id_c[0], C, bad), ra);
+#pragma unroll 1
+                for (uint64_t i = 0; i < n_chunks; ++i) {
+                    const bool more = i + 1 < n_chunks;
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        const uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
+                        const uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
+                        const bool ok2 = j + 2 < 8 || more;
+                        const uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
+                        Chunk<double> rb[2];
+                        gather(pin(idx1, S), rb);
+                        event(ra, S, Cprev, lr);
+                        const uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
+                        gather(pin(idx2, S), ra);
+                        event(rb, S, Cprev, lr);
+                        idx1 = idx3;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
+                    if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
+                }
+                ev += 8 * n_chunks;
+            }
+            while (ev < ev_end) {  // tail
+                Chunk<double> r[2];
+                gather(map_index(map, load_id(ev), C, bad), r);
+                event(r, S, Cprev, lr);
+                ++ev;
+            }
+            if (has_layer) ylt_row[t] = lr;  // A8, one entry per layer
+        }
+        if (BAL) {
+            __syncwarp();
+            uint64_t b = 0;
+            if (lane == 0) b = warps + atomicAdd(s.counter, 1ull);
+            ticket = __shfl_sync(0xffffffffu, b, 0) * B + gw;
+        } else if (s.counter) {
+            uint64_t next = 0;
+            if (c == 0) next = groups + atomicAdd(s.counter, 1ull);
+            ticket = __shfl_sync(gmask, next, lane - c);
+        } else {
+            ticket += groups;
+        }
+    }
+    if (bad) atomicOr(s.err, kErrRange);
+    if (s.counter) {  // the last block to finish resets the ticket counter for the next launch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(s.done, 1u) == gridDim.x - 1) {
+                *s.counter = 0;
+                *s.done = 0;
+                __threadfence();
+            }
+        }
+    }
+}
+
+template <int GU, bool BAL>
+cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
+                      int sm_count, cudaStream_t stream)
+{
+    static int occ = 0;
+    if (occ == 0) {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, portfolio_kernel<GU, BAL>, kScanThreads, 0);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    const uint64_t per_block = kScanThreads / GU;
+    const uint64_t max_blocks = (uint64_t)sm_count * occ;
+    const uint64_t rounds = (s.n_trials + max_blocks * per_block - 1) / (max_blocks * per_block);
+    const uint64_t slots = (s.n_trials + rounds - 1) / rounds;
+    uint64_t blocks = (slots + per_block - 1) / per_block;
+    if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
+    if (blocks > max_blocks) blocks = max_blocks;
+    portfolio_kernel<GU, BAL><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
+        s, d_map, us.d_rows, us.d_terms);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
+                             int sm_count, cudaStream_t stream, uint64_t *launches)
+{
+    if (s.n_trials == 0) return cudaSuccess;
+    ++*launches;
+    const bool bal = s.perm != nullptr;
+    switch (us.GU) {
+        case 2: return bal ? launch_pu<2, true>(us, d_map, s, sm_count, stream)
+                           : launch_pu<2, false>(us, d_map, s, sm_count, stream);
+        case 4: return bal ? launch_pu<4, true>(us, d_map, s, sm_count, stream)
+                           : launch_pu<4, false>(us, d_map, s, sm_count, stream);
+        case 8: return bal ? launch_pu<8, true>(us, d_map, s, sm_count, stream)
+                           : launch_pu<8, false>(us, d_map, s, sm_count, stream);
+        default: --*launches; return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace ara

@@ -1,0 +1,98 @@
+// scan_common.cuh -- device helpers shared by the scan kernels (scan.cu) and the union-row
+// portfolio kernel (portfolio.cu).  Internal to libara.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ara_internal.h"
+
+namespace ara {
+namespace scan_detail {
+
+constexpr int kScanThreads = 128;  // 4 warps: fine occupancy steps for 80-170 registers
+
+// One 32-byte chunk of a row: 4 doubles (fp64 store) or 8 floats (fp32 store, F3).
+template <typename R>
+struct Chunk {
+    static constexpr int N = 32 / (int)sizeof(R);
+    R v[N];
+};
+
+__device__ __forceinline__ void load_row_chunk(const double *p, Chunk<double> &r)
+{
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+        : "l"(p));
+}
+
+__device__ __forceinline__ void load_row_chunk(const float *p, Chunk<float> &r)
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+          "=f"(r.v[6]), "=f"(r.v[7])
+        : "l"(p));
+}
+
+// Separately rounded arithmetic in the store's precision (no FMA contraction).
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+
+__device__ __forceinline__ void load_ids8(const uint32_t *p, uint32_t (&v)[8])
+{
+    asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7])
+        : "l"(p));
+}
+
+__device__ __forceinline__ uint32_t load_id(const uint32_t *p)
+{
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t load_map(const uint32_t *p)
+{
+    uint32_t v;
+    asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// min(x, y) = (y < x ? y : x); max(x, 0) = (x < 0 ? 0 : x)   (the oracle's definitions)
+template <typename R>
+__device__ __forceinline__ R dmin(R x, R y) { return (y < x) ? y : x; }
+template <typename R>
+__device__ __forceinline__ R dmax0(R x) { return (x < R(0)) ? R(0) : x; }
+
+__device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, uint32_t id,
+                                              uint32_t C, bool &bad)
+{
+    const bool ok = (id - 1u) < C;  // id in [1, C]
+    bad |= !ok;
+    return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
+}
+
+// The row gather of event j+1 is issued while event j is computed.  `pin` gives the row index a
+// true data dependency on the running sum of the previous event (min with 2^32 - 1 - signbit(S),
+// which is 2^32 - 1 because S >= +0 and idx <= U < 2^32 - 1, so the value is unchanged): without
+// it ptxas hoists all eight gathers of an unrolled chunk and runs out of registers.
+__device__ __forceinline__ uint32_t pin(uint32_t idx, double S)
+{
+    const uint32_t sbit = (uint32_t)__double2hiint(S) >> 31;
+    return min(idx, 0xffffffffu - sbit);
+}
+
+__device__ __forceinline__ uint32_t pin(uint32_t idx, float S)
+{
+    const uint32_t sbit = __float_as_uint(S) >> 31;
+    return min(idx, 0xffffffffu - sbit);
+}
+
+}  // namespace scan_detail
+}  // namespace ara

@@ -27,10 +27,14 @@ def main():
     ap.add_argument("--flags", type=int, default=0, help="ara_run flags (4 = ARA_RUN_BALANCE)")
     ap.add_argument("--sched", default="", help="ARA_SCAN_SCHED: static | dynamic")
     ap.add_argument("--precision", type=int, default=64)
+    ap.add_argument("--env", action="append", default=[], help="KEY=VALUE set before the runs")
     args = ap.parse_args()
     import torch
 
     from paper_1308_2572_b200 import ara
+    for kv in args.env:
+        k, v = kv.split("=", 1)
+        os.environ[k] = v
     spec = datagen.PRESETS[args.config]
     ds = datagen.generate(spec)
     dev = torch.device("cuda:0")
@@ -69,7 +73,7 @@ def main():
         same = True if ref is None else bool(np.array_equal(out, ref))
         ref = out if ref is None else ref
         ms = float(np.median(ts))
-        print(json.dumps({"variant": v, "sched": args.sched or f"flags={args.flags}",
+        print(json.dumps({"variant": v, "env": args.env, "sched": args.sched or f"flags={args.flags}",
                           "config": args.config, "ms_median": ms,
                           "ms_min": float(min(ts)), "GBps_alg": bytes_alg / ms / 1e6,
                           "trial_events_per_s": n_ev * ds.n_layers / ms * 1e3,
