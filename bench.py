@@ -233,6 +233,9 @@ def main():
     # ---- inputs: ELTs/layers are identical on every rank (seeded); each rank generates only
     # its own trial slice of the YET (counter-based substreams), so the YET is never sent.
     ds = datagen.generate(spec, with_yet=False)
+    from paper_1308_2572_b200 import dist as adist
+    if world > 1:  # setup collective: rank 0's ELTs and terms reach every rank (NVLink)
+        adist.broadcast_inputs(ds, src=0)
     t0, t1 = partition(spec.n_trials, rank, world)
     n_loc = t1 - t0
     h_off_np = datagen.trial_offsets(spec, t0, n_loc)
@@ -256,8 +259,6 @@ def main():
     if rank == 0:
         log(f"[bench] {workload_name(spec)}; ranks {world}; local trials {n_loc}; "
             f"store {ctx.ara_get_info().store_bytes / 1e6:.1f} MB built in {t_store * 1e3:.1f} ms")
-
-    from paper_1308_2572_b200 import dist as adist
 
     def gather():
         if world == 1:
