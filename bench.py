@@ -316,12 +316,18 @@ def main():
     peak, peak_src = measured_peak()
     achieved = bytes_alg / (scan_ms * 1e-3) / 1e9
     traffic = None
+    physical = None
     prof = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            if pj.get("config") == spec.name and pj.get("n_trials") == n_loc:
-                traffic = pj.get("dram_bytes_per_launch")
+            pj = json.load(open(prof)).get(spec.name)
+            if pj and pj.get("n_trials") == n_loc and args.precision == 64:
+                traffic = pj["dram_bytes_per_launch"]
+                physical = {"bound": "l1_data_pipe (LSU wavefronts)",
+                            "l1_data_pipe_busy": pj["l1_data_pipe_busy"],
+                            "l2_throughput": pj["lts_throughput"],
+                            "dram_bytes_per_launch": traffic,
+                            "source": "ncu capture committed in profiles/ (same kernel, config)"}
         except Exception:
             pass
 
@@ -380,7 +386,8 @@ def main():
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                          "bytes_model": f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
-                                        "segment per event, YLT, offsets (north-star accounting)"},
+                                        "segment per event, YLT, offsets (north-star accounting)",
+                         "physical": physical},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
