@@ -169,7 +169,7 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     // nearly equal length (variable-length YETs keep full SIMT width; measured neutral for
     // equal lengths, profiles/README.md).  ARA_SCAN_SCHED=static|dynamic selects the plain
     // round-robin / per-group ticket schedules (tuning); the F4 outputs use per-group tickets.
-    const bool balance = ctx->sched == 0 && !extra;
+    const bool balance = ctx->sched == 0 && !extra && n <= 0xffffffffull;  // u32 permutation
     const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
     const uint32_t *perm = nullptr;
     if (balance) {
