@@ -96,15 +96,82 @@ __global__ void __launch_bounds__(256) k_coop(const uint32_t* __restrict__ ids, 
   }
 }
 
+
+// TMA variant: each group of 2 lanes keeps a ring of D row slots in shared memory; lane 0 issues a
+// 128-byte cp.async.bulk per event D-1 events ahead (mbarrier completion), both lanes wait and read
+// their 64 bytes with LDS.  Map lookups stay LDG.  (MODE 6: with map, 7: ids are row indices)
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(m)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"((uint32_t)__cvta_generic_to_shared(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }"
+               :: "r"((uint32_t)__cvta_generic_to_shared(m)), "r"(parity) : "memory");
+}
+
+template <int MODE, int D>   // D = ring slots per group (8): batches of 4 events issued one batch ahead
+__global__ void __launch_bounds__(128) k_tma(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ map,
+                       const double* __restrict__ rows, double* out, int n, int k) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double (*ring)[D][W] = reinterpret_cast<double (*)[D][W]>(smem);                 // [64][D][W]
+  uint64_t (*bar)[D] = reinterpret_cast<uint64_t (*)[D]>(smem + 64 * D * W * 8);  // [64][D]
+  const int lane = threadIdx.x & 31, c = lane & 1, gb = threadIdx.x >> 1;
+  const unsigned gmask = 3u << (lane - c);
+  if (c == 0) for (int s = 0; s < D; ++s) mbar_init(&bar[gb][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  uint32_t phase = 0;   // bit s = parity of slot s
+  int stride = gridDim.x * 64;
+  for (int t = blockIdx.x * 64 + gb; t < n; t += stride) {
+    const uint32_t* ev = ids + (size_t)t * k;
+    double acc = 0;
+    auto issue4 = [&](int d) {   // events d..d+3 (d multiple of 4)
+      if (c == 0 && d < k) {
+        uint4 q = *reinterpret_cast<const uint4*>(ev + d);
+        uint32_t id4[4] = {q.x, q.y, q.z, q.w};
+        #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t idx = MODE == 6 ? ldmap(map + id4[j]) : id4[j];
+          const int s = (d + j) % D;
+          mbar_expect_tx(&bar[gb][s], 128);
+          bulk_g2s(&ring[gb][s][0], rows + (size_t)idx * W, 128, &bar[gb][s]);
+        }
+      }
+    };
+    issue4(0);
+    for (int d = 0; d < k; d += 4) {
+      issue4(d + 4);
+      #pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int s = (d + j) % D;
+        mbar_wait(&bar[gb][s], (phase >> s) & 1);
+        phase ^= 1u << s;
+        const double4* p = reinterpret_cast<const double4*>(&ring[gb][s][8 * c]);
+        double4 a = p[0], b = p[1];
+        acc += a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+      }
+      __syncwarp(gmask);   // slots of this batch are reissued next iteration
+    }
+    out[(size_t)t * 2 + c] = acc;
+  }
+}
+
 template <typename K>
 void run(const char* name, K kern, int grid, const uint32_t* ids, const uint32_t* map, const double* rows,
-         double* out, int n, int k, bool map_used, bool row_used) {
+         double* out, int n, int k, bool map_used, bool row_used, int threads = 256, int smem = 0) {
+  if (smem) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
-  for (int w = 0; w < 2; ++w) kern<<<grid, 256>>>(ids, map, rows, out, n, k);
+  for (int w = 0; w < 2; ++w) kern<<<grid, threads, smem>>>(ids, map, rows, out, n, k);
   CK(cudaDeviceSynchronize());
   const int reps = 5;
   CK(cudaEventRecord(a));
-  for (int r = 0; r < reps; ++r) kern<<<grid, 256>>>(ids, map, rows, out, n, k);
+  for (int r = 0; r < reps; ++r) kern<<<grid, threads, smem>>>(ids, map, rows, out, n, k);
   CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
   float ms; CK(cudaEventElapsedTime(&ms, a, b)); ms /= reps;
   double ev = (double)n * k;
@@ -136,6 +203,12 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dmap, hmap.data(), (C + 1) * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(drows, hrows.data(), hrows.size() * 8, cudaMemcpyHostToDevice));
   printf("{\"sms\": %d, \"n\": %d, \"k\": %d, \"W\": %d}\n", sms, n, k, W);
+  CK(cudaMalloc(&dout, (size_t)n * 16));
+  for (int occ : {2, 3}) {
+    int grid = sms * occ;
+    run("tma_D8", k_tma<6, 8>, grid, dids, dmap, drows, dout, n, k, true, true, 128, 64 * 8 * (W * 8 + 8));
+    run("tma_D8_nomap", k_tma<7, 8>, grid, didx, dmap, drows, dout, n, k, false, true, 128, 64 * 8 * (W * 8 + 8));
+  }
   for (int occ : {4, 8}) {
     int grid = sms * occ;
     run("ids", k_lane<0>, grid, dids, dmap, drows, dout, n, k, false, false);
