@@ -118,6 +118,9 @@ for _k in (500, 2000):
     PRESETS[f"sweep-k{_k}"] = PRESETS["headline"].replace(name=f"sweep-k{_k}", k_min=_k, k_max=_k)
 PRESETS["sweep-ragged"] = PRESETS["headline"].replace(name="sweep-ragged", k_min=800, k_max=1500)
 PRESETS["sweep-n8m"] = PRESETS["headline"].replace(name="sweep-n8m", n_trials=8_000_000)
+# SURVEY.md 8(d) secondary workload: a global catalogue against a regional layer,
+# 10% of occurrences in the layer's pool, the rest absent from every ELT (zero rows).
+PRESETS["sweep-h10"] = PRESETS["headline"].replace(name="sweep-h10", hit=0.1)
 
 
 @dataclasses.dataclass

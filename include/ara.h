@@ -242,6 +242,10 @@ typedef struct {
     uint64_t kernel_launches;    /* kernels launched by this context so far               */
     int device;
     int sm_count;
+    int row_addressing;          /* how the scan finds an event's row:
+                                    0 = catalogue map -> dense row; 1 = rows indexed by
+                                    catalogue id; 2 = as 1 behind a shared-memory presence
+                                    bitmap.  Results are identical in every mode.          */
 } ara_info;
 
 ara_status ara_get_info(const ara_ctx *ctx, ara_info *out);

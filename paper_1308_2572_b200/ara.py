@@ -65,7 +65,8 @@ class Info(ctypes.Structure):
     _fields_ = [("catalogue_size", ctypes.c_uint32), ("n_elts", ctypes.c_uint32),
                 ("n_layers", ctypes.c_uint32), ("max_row_width", ctypes.c_uint32),
                 ("store_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("device", ctypes.c_int), ("sm_count", ctypes.c_int)]
+                ("device", ctypes.c_int), ("sm_count", ctypes.c_int),
+                ("row_addressing", ctypes.c_int)]
 
 
 def _load() -> ctypes.CDLL:

@@ -111,6 +111,9 @@ void free_layers(ara_ctx *ctx)
     cudaFree(ctx->store.d_terms);
     cudaFree(ctx->store.uni.d_rows);
     cudaFree(ctx->store.uni.d_terms);
+    cudaFree(ctx->store.uni.d_rows_direct);
+    cudaFree(ctx->store.d_rows_direct);
+    cudaFree(ctx->store.d_bitmap);
     ctx->store = ara::DeviceStore();
     ctx->store_bytes = 0;
     ctx->have_layers = false;
@@ -185,8 +188,9 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                       extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm};
     cudaError_t e =
         (ctx->store.uni.enabled && !extra)
-            ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, s, ctx->sm_count,
-                                    ctx->stream, &ctx->launches)
+            ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, ctx->store.map_mode,
+                                    ctx->store.d_bitmap, s, ctx->sm_count, ctx->stream,
+                                    &ctx->launches)
             : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
@@ -296,6 +300,49 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     if (e != cudaSuccess) return cuda_fail(ctx, e, "union store");
     us.enabled = true;
     ctx->store_bytes += row_bytes + sizeof(ut);
+    return ARA_OK;
+}
+
+// Map modes 1 and 2 (ara_internal.h): the rows the scan will read (union rows when the portfolio
+// kernel serves the layers, else the per-layer rows) expanded on the device to one row per
+// catalogue id, plus the presence bitmap for mode 2.  The direct rows are bit copies of the dense
+// ones (direct[id] = dense[map[id]]; absent ids get the zero row), so the YLT does not depend
+// on the mode.  Default mode 2; ARA_MAP_MODE=0|1|2 overrides (tuning).  The direct store costs
+// (C+1) row strides of HBM; when that exceeds a quarter of the free device memory the scan
+// stays on the map (mode 0).
+ara_status build_direct(ara_ctx *ctx)
+{
+    ara::DeviceStore &st = ctx->store;
+    int mode = 2;
+    if (const char *m = getenv("ARA_MAP_MODE")) mode = atoi(m);
+    if ((mode != 1 && mode != 2) || ctx->C == 0xffffffffu) return ARA_OK;  // ids < 2^32 - 1 (pin)
+    const bool uni = st.uni.enabled;
+    const size_t row_bytes = uni ? (size_t)8 * 8 * st.uni.GU
+                                 : (size_t)st.n_layers * st.width * (st.bits / 8);
+    const size_t bytes = ((size_t)ctx->C + 1) * row_bytes;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || bytes > free_b / 4) return ARA_OK;
+    void *direct = nullptr;
+    cudaError_t e = cudaMalloc(&direct, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return ARA_OK;  // stay on the map
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "direct store");
+    if (uni)
+        st.uni.d_rows_direct = (double *)direct;
+    else
+        st.d_rows_direct = direct;
+    e = ara::launch_expand_rows(st.d_map, ctx->C, uni ? (const void *)st.uni.d_rows : st.d_rows,
+                                direct, row_bytes, ctx->stream);
+    if (e == cudaSuccess && mode == 2) {
+        e = cudaMalloc(&st.d_bitmap, ara::kBitmapWords * 4);
+        if (e == cudaSuccess) e = ara::launch_build_bitmap(st.d_map, ctx->C, st.d_bitmap, ctx->stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "direct store");
+    st.map_mode = mode;
+    ctx->store_bytes += bytes + (mode == 2 ? ara::kBitmapWords * 4 : 0);
     return ARA_OK;
 }
 
@@ -512,6 +559,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         st.bits = ctx->bits;
         if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
+        if (const char *d = getenv("ARA_SCAN_DEPTH")) st.depth = atoi(d);
         std::vector<uint32_t> map((size_t)C + 1, 0u);
         std::vector<uint32_t> uni;
         for (uint32_t c = elt_offsets[0]; c < elt_offsets[n_layers]; ++c) {
@@ -550,6 +598,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         }
         ctx->store_bytes = map_bytes + row_bytes + term_bytes;
         ara_status us = build_union(ctx, map, terms, elt_offsets, elt_index);
+        if (us == ARA_OK) us = build_direct(ctx);
         if (us != ARA_OK) {
             free_layers(ctx);
             return us;
@@ -762,6 +811,7 @@ ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
     out->kernel_launches = ctx->launches;
     out->device = ctx->device;
     out->sm_count = ctx->sm_count;
+    out->row_addressing = ctx->have_layers ? ctx->store.map_mode : 0;
     return ARA_OK;
 }
 

@@ -80,6 +80,7 @@ struct UnionTermsDev {
 };
 struct UnionStore {
     bool enabled = false;
+    double *d_rows_direct = nullptr;     // [(C+1) * WU] rows by catalogue id (map mode >= 1)
     uint32_t GU = 0;         // lanes per trial (2, 4 or 8); union row width WU = 8 * GU doubles
     uint32_t n_cols = 0;     // |J|
     double *d_rows = nullptr;            // [(U+1) * WU]
@@ -97,11 +98,28 @@ struct DeviceStore {
     std::vector<uint32_t> n_cols;  // E of each layer
     int group_override = 0;      // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
     int min_blocks = 0;          // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
+    int depth = 0;               // tuning: rows in flight per group (env ARA_SCAN_DEPTH)
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
+    // Row addressing of the scan: 0 = through d_map (dense rows);
+    // 1 = direct (rows indexed by catalogue id, no map read); 2 = direct behind a presence
+    // bitmap held in shared memory (absent ids read the zero row instead of a cold line).
+    int map_mode = 0;
+    void *d_rows_direct = nullptr;  // [(C+1) * n_layers * W]: row id = dense row map[id]
+    uint32_t *d_bitmap = nullptr;   // [kBitmapWords]: bit h(id) set when map[id] != 0
     void *d_rows = nullptr;      // [(U+1) * n_layers * W] double or float, row 0 zero
     void *d_terms = nullptr;     // [n_layers] LayerTermsT<double or float>
     UnionStore uni;              // F1 union rows (when eligible)
 };
+
+// Presence bitmap of map mode 2: 2^19 bits (64 KB of shared memory per block, three blocks per
+// SM), bit h(id) = Fibonacci hash of the catalogue id.  A clear bit proves the id absent; a set
+// bit may be a collision (then the direct row, all zeros, is read).
+constexpr int kBitmapLog2 = 19;
+constexpr uint32_t kBitmapWords = 1u << (kBitmapLog2 - 5);
+__host__ __device__ inline uint32_t bitmap_hash(uint32_t id)
+{
+    return (id * 0x9E3779B1u) >> (32 - kBitmapLog2);
+}
 
 struct ScanLaunch {
     const uint64_t *offsets;  // [n+1], device
@@ -130,10 +148,17 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
                                cudaStream_t stream, uint64_t *launches);
 
 // scan.cu
+// Map modes >= 1: expand the dense rows to rows by catalogue id (direct[id] = dense[map[id]]) and
+// build the presence bitmap (mode 2).
+cudaError_t launch_expand_rows(const uint32_t *d_map, uint32_t C, const void *dense,
+                               void *direct, size_t row_bytes, cudaStream_t stream);
+cudaError_t launch_build_bitmap(const uint32_t *d_map, uint32_t C, uint32_t *bitmap,
+                                cudaStream_t stream);
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches);
-cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
-                             int sm_count, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int map_mode,
+                             const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
+                             cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
                             uint32_t catalogue_size, uint32_t *err, int sm_count,
                             cudaStream_t stream, uint64_t *launches);

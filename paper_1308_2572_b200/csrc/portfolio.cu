@@ -36,11 +36,14 @@ __host__ __device__ constexpr int u_row_doubles()
     return (u_slot(8 * GU) + 2 + 15) / 16 * 16 + 1;
 }
 
-template <int GU, bool BAL>
+template <int GU, bool BAL, int MM>
 __global__ void __launch_bounds__(kScanThreads, 3)
     portfolio_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                     const double *__restrict__ urows, const UnionTermsDev *__restrict__ ut)
+                     const uint32_t *__restrict__ bitmap, const double *__restrict__ urows,
+                     const UnionTermsDev *__restrict__ ut)
 {
+    extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
+    load_bitmap<MM>(sbits, bitmap);
     constexpr int WU = 8 * GU;              // union row width (doubles)
     constexpr int GS = u_row_doubles<GU>(); // shared F row stride per group (doubles)
     constexpr int ZERO = u_slot(WU);        // index of the zero pair
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             double S = 0.0, Cprev = 0.0, lr = 0.0;
             while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {  // unaligned head
                 Chunk<double> r[2];
-                gather(map_index(map, load_id(ev), C, bad), r);
+                gather(row_index<MM>(map, sbits, load_id(ev), C, bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -146,9 +149,9 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                 uint32_t id_c[8], id_n[8];
                 load_ids8(ev, id_c);
                 if (n_chunks > 1) load_ids8(ev + 8, id_n);
-                uint32_t idx1 = map_index(map, id_c[1], C, bad);
+                uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, bad);
                 Chunk<double> ra[2];
-                gather(map_index(map, id_c[0], C, bad), ra);
+                gather(row_index<MM>(map, sbits, id_c[0], C, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -157,11 +160,11 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                         const uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                         const uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                         const bool ok2 = j + 2 < 8 || more;
-                        const uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
                         Chunk<double> rb[2];
                         gather(pin(idx1, S), rb);
                         event(ra, S, Cprev, lr);
-                        const uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
+                        const uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, bad) : 0u;
                         gather(pin(idx2, S), ra);
                         event(rb, S, Cprev, lr);
                         idx1 = idx3;
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             }
             while (ev < ev_end) {  // tail
                 Chunk<double> r[2];
-                gather(map_index(map, load_id(ev), C, bad), r);
+                gather(row_index<MM>(map, sbits, load_id(ev), C, bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -207,14 +210,19 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     }
 }
 
-template <int GU, bool BAL>
-cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
-                      int sm_count, cudaStream_t stream)
+template <int GU, bool BAL, int MM>
+cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32_t *d_bitmap,
+                       const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
+    const size_t smem = MM == 2 ? kBitmapWords * 4 : 0;
     static int occ = 0;
     if (occ == 0) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, portfolio_kernel<GU, BAL>, kScanThreads, 0);
+        cudaError_t e = cudaFuncSetAttribute(portfolio_kernel<GU, BAL, MM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, portfolio_kernel<GU, BAL, MM>,
+                                                          kScanThreads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -225,26 +233,37 @@ cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, const ScanLau
     uint64_t blocks = (slots + per_block - 1) / per_block;
     if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
     if (blocks > max_blocks) blocks = max_blocks;
-    portfolio_kernel<GU, BAL><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
-        s, d_map, us.d_rows, us.d_terms);
+    portfolio_kernel<GU, BAL, MM><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
+        s, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();
+}
+
+template <int GU, bool BAL>
+cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, int map_mode,
+                      const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
+                      cudaStream_t stream)
+{
+    if (map_mode == 1) return launch_pum<GU, BAL, 1>(us, d_map, d_bitmap, s, sm_count, stream);
+    if (map_mode == 2) return launch_pum<GU, BAL, 2>(us, d_map, d_bitmap, s, sm_count, stream);
+    return launch_pum<GU, BAL, 0>(us, d_map, d_bitmap, s, sm_count, stream);
 }
 
 }  // namespace
 
-cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, const ScanLaunch &s,
-                             int sm_count, cudaStream_t stream, uint64_t *launches)
+cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int map_mode,
+                             const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
+                             cudaStream_t stream, uint64_t *launches)
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
     const bool bal = s.perm != nullptr;
     switch (us.GU) {
-        case 2: return bal ? launch_pu<2, true>(us, d_map, s, sm_count, stream)
-                           : launch_pu<2, false>(us, d_map, s, sm_count, stream);
-        case 4: return bal ? launch_pu<4, true>(us, d_map, s, sm_count, stream)
-                           : launch_pu<4, false>(us, d_map, s, sm_count, stream);
-        case 8: return bal ? launch_pu<8, true>(us, d_map, s, sm_count, stream)
-                           : launch_pu<8, false>(us, d_map, s, sm_count, stream);
+        case 2: return bal ? launch_pu<2, true>(us, d_map, map_mode, d_bitmap, s, sm_count, stream)
+                           : launch_pu<2, false>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        case 4: return bal ? launch_pu<4, true>(us, d_map, map_mode, d_bitmap, s, sm_count, stream)
+                           : launch_pu<4, false>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        case 8: return bal ? launch_pu<8, true>(us, d_map, map_mode, d_bitmap, s, sm_count, stream)
+                           : launch_pu<8, false>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
     }
 }

@@ -98,12 +98,14 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
     for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
 }
 
-template <int G, int CH, int MINB, bool X, typename R, bool BAL>
+template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D = 2>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                const R *__restrict__ rows, const LayerTermsT<R> *__restrict__ terms,
-                uint32_t n_layers)
+                const uint32_t *__restrict__ bitmap, const R *__restrict__ rows,
+                const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
 {
+    extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
+    load_bitmap<MM>(sbits, bitmap);
     constexpr int PER = Chunk<R>::N;
     constexpr int W = PER * G * CH;  // row width per layer (elements)
     constexpr int NCOL = PER * CH;   // columns per lane
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -187,12 +189,45 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // during chunk i (one 32-byte load per chunk), the map lookup of event j+2 and the row
         // gather of event j+1 are in flight while event j is computed.
         const uint64_t n_chunks = (uint64_t)(ev_end - ev) / 8;
-        if (n_chunks) {
+        if constexpr (D > 2) {
+            // Deep pipeline: a ring of D row buffers; event j is computed from slot j % D, which
+            // is then refilled with the row of event j + D (zero row past the trial's end).
+            static_assert(8 % D == 0, "D divides the 8-event chunk");
+            if (n_chunks) {
+                uint32_t id_c[8], id_n[8];
+                load_ids8(ev, id_c);
+                if (n_chunks > 1) load_ids8(ev + 8, id_n);
+                Chunk<R> ring[D][CH];
+#pragma unroll
+                for (int e = 0; e < D; ++e)
+                    gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, id_c[e], C, bad),
+                                  ring[e]);
+#pragma unroll 1
+                for (uint64_t i = 0; i < n_chunks; ++i) {
+                    const bool more = i + 1 < n_chunks;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        event_step<G, CH, R>(ring[j % D], rate, ret, lim, gmask, occ_ret, occ_lim,
+                                             agg_ret, agg_lim, S, Cprev, lr, oc, inc);
+                        event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
+                        const int e2 = j + D;  // refill: event j + D of this chunk or the next
+                        const uint32_t id2 = e2 < 8 ? id_c[e2 < 8 ? e2 : 0] : id_n[e2 < 8 ? 0 : e2 - 8];
+                        const bool ok2 = e2 < 8 || more;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
+                        gather<CH, R>(my_rows, row_stride, pin(idx2, S), ring[j % D]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
+                    if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
+                }
+                ev += 8 * n_chunks;
+            }
+        } else if (n_chunks) {
             uint32_t id_c[8], id_n[8];
             load_ids8(ev, id_c);
             if (n_chunks > 1) load_ids8(ev + 8, id_n);
-            uint32_t idx0 = map_index(map, id_c[0], C, bad);
-            uint32_t idx1 = map_index(map, id_c[1], C, bad);
+            uint32_t idx0 = row_index<MM>(map, sbits, id_c[0], C, bad);
+            uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, bad);
             Chunk<R> ra[CH];
             gather<CH, R>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
@@ -204,13 +239,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                     uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                     const bool ok2 = j + 2 < 8 || more;
-                    uint32_t idx2 = ok2 ? map_index(map, id2, C, bad) : 0u;
+                    uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
                     Chunk<R> rb[CH];
                     gather<CH, R>(my_rows, row_stride, pin(idx1, S), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
                     event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
-                    uint32_t idx3 = ok2 ? map_index(map, id3, C, bad) : 0u;
+                    uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, bad) : 0u;
                     gather<CH, R>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
@@ -226,7 +261,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // tail: remaining events one by one
         while (ev < ev_end) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, map_index(map, load_id(ev), C, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -296,14 +331,19 @@ __global__ void length_keys_kernel(const uint64_t *__restrict__ offsets, uint64_
     }
 }
 
-template <int G, int CH, int MINB = 1, bool X = false, typename R = double, bool BAL = false>
-cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
-                      cudaStream_t stream)
+template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D>
+cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                       cudaStream_t stream)
 {
+    const size_t smem = MM == 2 ? kBitmapWords * 4 : 0;
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, scan_kernel<G, CH, MINB, X, R, BAL>, kScanThreads, 0);
+        cudaError_t e = cudaFuncSetAttribute(scan_kernel<G, CH, MINB, X, R, BAL, MM, D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &occ, scan_kernel<G, CH, MINB, X, R, BAL, MM, D>, kScanThreads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
     }
@@ -326,12 +366,66 @@ cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
         blocks = (blocks + lcm - 1) / lcm * lcm;
     if (blocks > max_blocks) blocks = max_blocks;
-    scan_kernel<G, CH, MINB, X, R, BAL><<<(unsigned)blocks, kScanThreads, 0, stream>>>(
-        s, st.d_map, (const R *)st.d_rows, (const LayerTermsT<R> *)st.d_terms, st.n_layers);
+    scan_kernel<G, CH, MINB, X, R, BAL, MM, D><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
+        s, st.d_map, st.d_bitmap, (const R *)(MM ? st.d_rows_direct : st.d_rows),
+        (const LayerTermsT<R> *)st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
 
+// Map mode dispatch; the F4 outputs (X) always use the dense rows through the map.
+template <int G, int CH, int MINB = 1, bool X = false, typename R = double, bool BAL = false,
+          int D = 2>
+cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                      cudaStream_t stream)
+{
+    if (!X && st.map_mode == 1)
+        return launch_gcm<G, CH, MINB, X, R, BAL, X ? 0 : 1, D>(st, s, sm_count, stream);
+    if (!X && st.map_mode == 2)
+        return launch_gcm<G, CH, MINB, X, R, BAL, X ? 0 : 2, D>(st, s, sm_count, stream);
+    return launch_gcm<G, CH, MINB, X, R, BAL, 0, D>(st, s, sm_count, stream);
+}
+
 }  // namespace
+
+__global__ void expand_rows_kernel(const uint32_t *__restrict__ map, uint32_t C,
+                                   const uint4 *__restrict__ dense, uint4 *__restrict__ direct,
+                                   uint32_t row_vecs)
+{
+    const uint64_t n = ((uint64_t)C + 1) * row_vecs;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = i / row_vecs, v = i - id * row_vecs;
+        direct[i] = dense[(uint64_t)map[id] * row_vecs + v];
+    }
+}
+
+__global__ void build_bitmap_kernel(const uint32_t *__restrict__ map, uint32_t C, uint32_t *bits)
+{
+    for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x + 1; id <= C && id != 0;
+         id += gridDim.x * blockDim.x)
+        if (map[id]) {
+            const uint32_t h = bitmap_hash(id);
+            atomicOr(bits + (h >> 5), 1u << (h & 31u));
+        }
+}
+
+cudaError_t launch_expand_rows(const uint32_t *d_map, uint32_t C, const void *dense,
+                               void *direct, size_t row_bytes, cudaStream_t stream)
+{
+    if (row_bytes % 16) return cudaErrorInvalidValue;
+    expand_rows_kernel<<<1184, 256, 0, stream>>>(d_map, C, (const uint4 *)dense, (uint4 *)direct,
+                                                 (uint32_t)(row_bytes / 16));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_bitmap(const uint32_t *d_map, uint32_t C, uint32_t *bitmap,
+                                cudaStream_t stream)
+{
+    cudaError_t e = cudaMemsetAsync(bitmap, 0, kBitmapWords * 4, stream);
+    if (e != cudaSuccess) return e;
+    build_bitmap_kernel<<<592, 256, 0, stream>>>(d_map, C, bitmap);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches)
@@ -351,7 +445,19 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
         switch (st.width) {
             case 4: return launch_gc<1, 1, 1, false, double, true>(st, s, sm_count, stream);
             case 8: return launch_gc<2, 1, 1, false, double, true>(st, s, sm_count, stream);
-            case 16: return launch_gc<2, 2, 3, false, double, true>(st, s, sm_count, stream);
+            case 16:  // tuning variants: ARA_SCAN_GROUP (G), ARA_SCAN_DEPTH (D), ARA_SCAN_MINB
+                if (st.group_override == 4) {
+                    if (st.depth == 8)
+                        return launch_gc<4, 1, 3, false, double, true, 8>(st, s, sm_count, stream);
+                    if (st.min_blocks == 4)
+                        return launch_gc<4, 1, 4, false, double, true, 4>(st, s, sm_count, stream);
+                    return launch_gc<4, 1, 3, false, double, true, 4>(st, s, sm_count, stream);
+                }
+                if (st.depth == 4)
+                    return launch_gc<2, 2, 2, false, double, true, 4>(st, s, sm_count, stream);
+                if (st.min_blocks == 2)
+                    return launch_gc<2, 2, 2, false, double, true>(st, s, sm_count, stream);
+                return launch_gc<2, 2, 3, false, double, true>(st, s, sm_count, stream);
             case 32: return launch_gc<4, 2, 1, false, double, true>(st, s, sm_count, stream);
             case 48: return launch_gc<4, 3, 1, false, double, true>(st, s, sm_count, stream);
             case 64: return launch_gc<4, 4, 1, false, double, true>(st, s, sm_count, stream);

@@ -78,19 +78,51 @@ __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, 
     return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
 }
 
-// The row gather of event j+1 is issued while event j is computed.  `pin` gives the row index a
-// true data dependency on the running sum of the previous event (min with 2^32 - 1 - signbit(S),
-// which is 2^32 - 1 because S >= +0 and idx <= U < 2^32 - 1, so the value is unchanged): without
-// it ptxas hoists all eight gathers of an unrolled chunk and runs out of registers.
-__device__ __forceinline__ uint32_t pin(uint32_t idx, double S)
+// A3 for every map mode (ara_internal.h DeviceStore::map_mode): the row that holds catalogue id
+// `id`'s losses.  0: dense row map[id] (one 4-byte L2 read per event); 1: row id of the direct
+// store (no read: the L1 data pipe is the scan's binding resource and the map read was a third
+// of its wavefronts); 2: as 1 behind the shared-memory presence bitmap `sbits`, so absent ids
+// read the one zero row instead of a cold line of the direct store.  Out-of-range ids read the
+// zero row and raise `bad`.
+template <int MM>
+__device__ __forceinline__ uint32_t row_index(const uint32_t *__restrict__ map,
+                                              const uint32_t *sbits, uint32_t id, uint32_t C,
+                                              bool &bad)
 {
-    const uint32_t sbit = (uint32_t)__double2hiint(S) >> 31;
+    const bool ok = (id - 1u) < C;  // id in [1, C]
+    bad |= !ok;
+    if (MM == 0) return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
+    if (MM == 1) return ok ? id : 0u;
+    const uint32_t h = bitmap_hash(id);
+    const uint32_t w = sbits[h >> 5];
+    return (ok && ((w >> (h & 31u)) & 1u)) ? id : 0u;
+}
+
+// Mode 2: copy the presence bitmap into this block's shared memory (64 KB, 16-byte loads).
+template <int MM>
+__device__ __forceinline__ void load_bitmap(uint32_t *sbits, const uint32_t *__restrict__ bitmap)
+{
+    if (MM != 2) return;
+    const uint4 *src = reinterpret_cast<const uint4 *>(bitmap);
+    uint4 *dst = reinterpret_cast<uint4 *>(sbits);
+    for (uint32_t i = threadIdx.x; i < kBitmapWords / 4; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+}
+
+// A row gather is issued only after the values it will overwrite have been consumed: `pin`
+// gives the row index a true data dependency on such a value v (min with 2^32 - 1 - signbit(v),
+// which leaves every row index unchanged because indices are < 2^32 - 1); without it ptxas
+// hoists the gathers of an unrolled chunk above the arithmetic that frees their registers and
+// runs out of registers.
+__device__ __forceinline__ uint32_t pin(uint32_t idx, double v)
+{
+    const uint32_t sbit = (uint32_t)__double2hiint(v) >> 31;
     return min(idx, 0xffffffffu - sbit);
 }
 
-__device__ __forceinline__ uint32_t pin(uint32_t idx, float S)
+__device__ __forceinline__ uint32_t pin(uint32_t idx, float v)
 {
-    const uint32_t sbit = __float_as_uint(S) >> 31;
+    const uint32_t sbit = __float_as_uint(v) >> 31;
     return min(idx, 0xffffffffu - sbit);
 }
 

@@ -193,6 +193,37 @@ def test_absent_events_only(stream):
     assert_bit_identical(gpu_ylt(ds, stream), want)
 
 
+# --------------------------------------------------------------------------- row addressing
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("preset,kw", [
+    ("tiny", dict(n_trials=900, k_min=0, k_max=40)),                    # h = 0.5, C = 1000
+    ("sweep-h10", dict(n_trials=1200, k_min=990, k_max=1010)),          # 90% absent ids, C = 2M
+    ("portfolio", dict(n_trials=400, k_min=100, k_max=300)),            # union-row kernel
+    ("sweep-e32", dict(n_trials=600, k_min=200, k_max=260)),
+    ("tiny", dict(n_trials=500, k_min=50, k_max=300, catalogue_size=(1 << 21) + 777,
+                  pool_size=30_000, records_per_elt=20_000)),  # ~6% of absent ids alias a set bit
+])
+def test_row_addressing_modes(stream, monkeypatch, mode, preset, kw):
+    """Every row-addressing mode (catalogue map, rows by catalogue id, id rows behind the
+    shared-memory presence bitmap) gives the oracle's YLT bit for bit, including catalogues larger
+    than the bitmap (hash collisions read the direct store's zero rows) and out-of-pool ids."""
+    monkeypatch.setenv("ARA_MAP_MODE", str(mode))
+    ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
+    if ds.catalogue_size > (1 << 21):  # the case is meant to exercise bitmap collisions
+        h = lambda ids: (ids.astype(np.uint64) * 0x9E3779B1 % (1 << 32)) >> 13  # noqa: E731
+        present = np.zeros(ds.catalogue_size + 1, bool)
+        present[ds.rec_event_ids] = True
+        bits = np.zeros(1 << 19, bool)
+        bits[h(np.flatnonzero(present))] = True
+        assert (bits[h(ds.events)] & ~present[ds.events]).sum() > 100
+    want = oracle.run_analysis(ds, n_threads=8)
+    ctx = make_ctx(ds, stream)
+    assert ctx.ara_get_info().row_addressing == mode
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx), want)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
+    ctx.close()
+
+
 # --------------------------------------------------------------------------- store (A1)
 @pytest.mark.parametrize("preset", ["tiny", "medium"])
 def test_store_round_trip(stream, preset):

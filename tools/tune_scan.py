@@ -47,9 +47,11 @@ def main():
     bytes_alg = n_ev * (4 + args.precision // 8 * E * L) + 8 * n * L + 8 * (n + 1)
     ref = None
     for v in args.variants.split(","):
-        g, mb = v.split(":")
+        g, mb, *mm = v.split(":")  # G:MINB[:ARA_MAP_MODE]
         os.environ["ARA_SCAN_GROUP"] = g
         os.environ["ARA_SCAN_MINB"] = mb
+        if mm:
+            os.environ["ARA_MAP_MODE"] = mm[0]
         os.environ["ARA_SCAN_SCHED"] = args.sched
         ctx = ara.Context(0, stream)
         ctx.ara_set_precision(args.precision)
