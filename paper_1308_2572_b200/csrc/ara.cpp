@@ -182,6 +182,7 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
         perm = ctx->sort.perm;
     }
     ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
+                      0u,  // zero_base: set per launch from the store the kernel reads
                       dyn ? ctx->d_ticket : nullptr,
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
@@ -206,7 +207,7 @@ void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vecto
 {
     const uint32_t n_layers = st.n_layers, W = st.width;
     const size_t stride = (size_t)n_layers * W;
-    rows_buf.assign((size_t)(st.n_union + 1) * stride * sizeof(R), 0);
+    rows_buf.assign((size_t)(st.n_union + 1 + ara::kZeroRows) * stride * sizeof(R), 0);
     terms_buf.assign((size_t)n_layers * sizeof(ara::LayerTermsT<R>), 0);
     R *rows = (R *)rows_buf.data();
     ara::LayerTermsT<R> *lt = (ara::LayerTermsT<R> *)terms_buf.data();
@@ -260,7 +261,7 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     if (GU > 8) return ARA_OK;
     const uint32_t WU = 8 * GU;
     auto u_slot = [](uint32_t col) { return col + 2 * (col >> 3); };
-    std::vector<double> rows((size_t)(st.n_union + 1) * WU, 0.0);
+    std::vector<double> rows((size_t)(st.n_union + 1 + ara::kZeroRows) * WU, 0.0);
     ara::UnionTermsDev ut{};
     for (uint32_t col = 0; col < WU; ++col) {  // padding columns: neutral terms, zero losses
         ut.rate[col] = 1.0;
@@ -292,6 +293,7 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     ara::UnionStore &us = st.uni;
     us.GU = GU;
     us.n_cols = (uint32_t)J.size();
+    us.zero_base = st.n_union + 1;
     const size_t row_bytes = rows.size() * 8;
     cudaError_t e = cudaMalloc(&us.d_rows, row_bytes);
     if (e == cudaSuccess) e = cudaMalloc(&us.d_terms, sizeof(ut));
@@ -315,11 +317,12 @@ ara_status build_direct(ara_ctx *ctx)
     ara::DeviceStore &st = ctx->store;
     int mode = 2;
     if (const char *m = getenv("ARA_MAP_MODE")) mode = atoi(m);
-    if ((mode != 1 && mode != 2) || ctx->C == 0xffffffffu) return ARA_OK;  // ids < 2^32 - 1 (pin)
+    // row indices (ids and the zero-row block after them) stay below 2^32 - 1 (pin)
+    if ((mode != 1 && mode != 2) || ctx->C > 0xfffffffeu - ara::kZeroRows - 1) return ARA_OK;
     const bool uni = st.uni.enabled;
     const size_t row_bytes = uni ? (size_t)8 * 8 * st.uni.GU
                                  : (size_t)st.n_layers * st.width * (st.bits / 8);
-    const size_t bytes = ((size_t)ctx->C + 1) * row_bytes;
+    const size_t bytes = ((size_t)ctx->C + 1 + ara::kZeroRows) * row_bytes;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || bytes > free_b / 4) return ARA_OK;
     void *direct = nullptr;
@@ -342,6 +345,8 @@ ara_status build_direct(ara_ctx *ctx)
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "direct store");
     st.map_mode = mode;
+    st.zero_base_direct = ctx->C + 1;
+    st.uni.zero_base_direct = ctx->C + 1;
     ctx->store_bytes += bytes + (mode == 2 ? ara::kBitmapWords * 4 : 0);
     return ARA_OK;
 }
@@ -574,6 +579,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         }
         std::sort(uni.begin(), uni.end());
         st.n_union = (uint32_t)uni.size();
+        st.zero_base = st.n_union + 1;
         for (uint32_t u = 0; u < st.n_union; ++u) map[uni[u]] = u + 1;
         size_t row_bytes = 0, term_bytes = 0;
         std::vector<char> rows_buf, terms_buf;

@@ -80,10 +80,12 @@ struct UnionTermsDev {
 };
 struct UnionStore {
     bool enabled = false;
-    double *d_rows_direct = nullptr;     // [(C+1) * WU] rows by catalogue id (map mode >= 1)
+    double *d_rows_direct = nullptr;     // [(C+1+kZeroRows) * WU] rows by catalogue id (mode >= 1)
+    uint32_t zero_base = 0;              // U + 1: zero-row block of d_rows
+    uint32_t zero_base_direct = 0;       // C + 1: zero-row block of d_rows_direct
     uint32_t GU = 0;         // lanes per trial (2, 4 or 8); union row width WU = 8 * GU doubles
     uint32_t n_cols = 0;     // |J|
-    double *d_rows = nullptr;            // [(U+1) * WU]
+    double *d_rows = nullptr;            // [(U+1+kZeroRows) * WU]
     UnionTermsDev *d_terms = nullptr;
 };
 
@@ -104,12 +106,21 @@ struct DeviceStore {
     // 1 = direct (rows indexed by catalogue id, no map read); 2 = direct behind a presence
     // bitmap held in shared memory (absent ids read the zero row instead of a cold line).
     int map_mode = 0;
-    void *d_rows_direct = nullptr;  // [(C+1) * n_layers * W]: row id = dense row map[id]
+    void *d_rows_direct = nullptr;  // [(C+1+kZeroRows) * n_layers * W]: row id = dense map[id]
     uint32_t *d_bitmap = nullptr;   // [kBitmapWords]: bit h(id) set when map[id] != 0
-    void *d_rows = nullptr;      // [(U+1) * n_layers * W] double or float, row 0 zero
+    void *d_rows = nullptr;      // [(U+1+kZeroRows) * n_layers * W] double or float; row 0 and
+                                 // rows U+1.. (the zero-row block) are zero
+    uint32_t zero_base = 0;      // U + 1
+    uint32_t zero_base_direct = 0;  // C + 1 (d_rows_direct)
     void *d_terms = nullptr;     // [n_layers] LayerTermsT<double or float>
     UnionStore uni;              // F1 union rows (when eligible)
 };
+
+// Every row store ends with a block of kZeroRows all-zero rows (at DeviceStore / UnionStore
+// zero_base): an absent or out-of-range id reads zero row zero_base + (id mod kZeroRows), so the
+// reads of absent events spread over many L2 lines instead of all hitting row 0's line (the row
+// gathers bypass L1, so a single shared zero line would be one hot L2 slice).
+constexpr uint32_t kZeroRows = 1024;
 
 // Presence bitmap of map mode 2: 2^19 bits (64 KB of shared memory per block, three blocks per
 // SM), bit h(id) = Fibonacci hash of the catalogue id.  A clear bit proves the id absent; a set
@@ -129,6 +140,7 @@ struct ScanLaunch {
     uint64_t n_trials;
     uint32_t catalogue_size;
     uint32_t *err;            // device error word (bit 0: id out of range)
+    uint32_t zero_base;       // first row of the zero-row block of the rows the kernel reads
     unsigned long long *counter;  // dynamic ticket counter (NULL: static assignment)
     unsigned int *done;           // finished-block counter (resets `counter`)
     double *max_occ;              // F4: [n_layers][max_occ_ld] or NULL

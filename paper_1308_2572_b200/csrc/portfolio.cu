@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     double *const ylt_row = s.ylt + (size_t)ly * s.ylt_ld;
     const double *__restrict__ my_rows = urows + 4 * c;
     const uint32_t C = s.catalogue_size;
+    const uint32_t zb = s.zero_base;
     __syncwarp();
 
     // one event: F of this lane's columns -> shared row -> this lane's layer sum and state
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             double S = 0.0, Cprev = 0.0, lr = 0.0;
             while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {  // unaligned head
                 Chunk<double> r[2];
-                gather(row_index<MM>(map, sbits, load_id(ev), C, bad), r);
+                gather(row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -149,9 +150,9 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                 uint32_t id_c[8], id_n[8];
                 load_ids8(ev, id_c);
                 if (n_chunks > 1) load_ids8(ev + 8, id_n);
-                uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, bad);
+                uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, zb, bad);
                 Chunk<double> ra[2];
-                gather(row_index<MM>(map, sbits, id_c[0], C, bad), ra);
+                gather(row_index<MM>(map, sbits, id_c[0], C, zb, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -160,11 +161,11 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                         const uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                         const uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                         const bool ok2 = j + 2 < 8 || more;
-                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
                         Chunk<double> rb[2];
                         gather(pin(idx1, S), rb);
                         event(ra, S, Cprev, lr);
-                        const uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, bad) : 0u;
+                        const uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, zb, bad) : zb;
                         gather(pin(idx2, S), ra);
                         event(rb, S, Cprev, lr);
                         idx1 = idx3;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             }
             while (ev < ev_end) {  // tail
                 Chunk<double> r[2];
-                gather(row_index<MM>(map, sbits, load_id(ev), C, bad), r);
+                gather(row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -233,8 +234,10 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
     uint64_t blocks = (slots + per_block - 1) / per_block;
     if (blocks >= (uint64_t)sm_count) blocks = (blocks + sm_count - 1) / sm_count * sm_count;
     if (blocks > max_blocks) blocks = max_blocks;
+    ScanLaunch sl = s;
+    sl.zero_base = MM ? us.zero_base_direct : us.zero_base;
     portfolio_kernel<GU, BAL, MM><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
-        s, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
+        sl, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();
 }
 

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     const uint32_t leader = lane - c;
     const uint32_t row_stride = n_layers * W;  // elements per union row
     const uint32_t C = s.catalogue_size;
+    const uint32_t zb = s.zero_base;
 
     R rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
     R occ_ret = 0, occ_lim = 0, agg_ret = 0, agg_lim = 0;
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                 Chunk<R> ring[D][CH];
 #pragma unroll
                 for (int e = 0; e < D; ++e)
-                    gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, id_c[e], C, bad),
+                    gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, id_c[e], C, zb, bad),
                                   ring[e]);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                         const int e2 = j + D;  // refill: event j + D of this chunk or the next
                         const uint32_t id2 = e2 < 8 ? id_c[e2 < 8 ? e2 : 0] : id_n[e2 < 8 ? 0 : e2 - 8];
                         const bool ok2 = e2 < 8 || more;
-                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
                         gather<CH, R>(my_rows, row_stride, pin(idx2, S), ring[j % D]);
                     }
 #pragma unroll
@@ -226,8 +227,8 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             uint32_t id_c[8], id_n[8];
             load_ids8(ev, id_c);
             if (n_chunks > 1) load_ids8(ev + 8, id_n);
-            uint32_t idx0 = row_index<MM>(map, sbits, id_c[0], C, bad);
-            uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, bad);
+            uint32_t idx0 = row_index<MM>(map, sbits, id_c[0], C, zb, bad);
+            uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, zb, bad);
             Chunk<R> ra[CH];
             gather<CH, R>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
@@ -239,13 +240,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                     uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                     const bool ok2 = j + 2 < 8 || more;
-                    uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, bad) : 0u;
+                    uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
                     Chunk<R> rb[CH];
                     gather<CH, R>(my_rows, row_stride, pin(idx1, S), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
                     event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
-                    uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, bad) : 0u;
+                    uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, zb, bad) : zb;
                     gather<CH, R>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // tail: remaining events one by one
         while (ev < ev_end) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -366,8 +367,10 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks >= (uint64_t)sm_count && (blocks + lcm - 1) / lcm * lcm <= max_blocks)
         blocks = (blocks + lcm - 1) / lcm * lcm;
     if (blocks > max_blocks) blocks = max_blocks;
+    ScanLaunch sl = s;
+    sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     scan_kernel<G, CH, MINB, X, R, BAL, MM, D><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
-        s, st.d_map, st.d_bitmap, (const R *)(MM ? st.d_rows_direct : st.d_rows),
+        sl, st.d_map, st.d_bitmap, (const R *)(MM ? st.d_rows_direct : st.d_rows),
         (const LayerTermsT<R> *)st.d_terms, st.n_layers);
     return cudaGetLastError();
 }
@@ -391,11 +394,12 @@ __global__ void expand_rows_kernel(const uint32_t *__restrict__ map, uint32_t C,
                                    const uint4 *__restrict__ dense, uint4 *__restrict__ direct,
                                    uint32_t row_vecs)
 {
-    const uint64_t n = ((uint64_t)C + 1) * row_vecs;
+    // rows 0..C: direct[id] = dense[map[id]]; rows C+1..C+kZeroRows: the zero-row block
+    const uint64_t n = ((uint64_t)C + 1 + kZeroRows) * row_vecs;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t id = i / row_vecs, v = i - id * row_vecs;
-        direct[i] = dense[(uint64_t)map[id] * row_vecs + v];
+        direct[i] = id <= C ? dense[(uint64_t)map[id] * row_vecs + v] : make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -458,9 +462,15 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
                 if (st.min_blocks == 2)
                     return launch_gc<2, 2, 2, false, double, true>(st, s, sm_count, stream);
                 return launch_gc<2, 2, 3, false, double, true>(st, s, sm_count, stream);
-            case 32: return launch_gc<4, 2, 1, false, double, true>(st, s, sm_count, stream);
+            case 32:
+                if (st.group_override == 8)
+                    return launch_gc<8, 1, 4, false, double, true>(st, s, sm_count, stream);
+                return launch_gc<4, 2, 1, false, double, true>(st, s, sm_count, stream);
             case 48: return launch_gc<4, 3, 1, false, double, true>(st, s, sm_count, stream);
-            case 64: return launch_gc<4, 4, 1, false, double, true>(st, s, sm_count, stream);
+            case 64:
+                if (st.group_override == 8)
+                    return launch_gc<8, 2, 3, false, double, true>(st, s, sm_count, stream);
+                return launch_gc<4, 4, 1, false, double, true>(st, s, sm_count, stream);
             default: --*launches; return cudaErrorInvalidValue;
         }
     }

@@ -21,14 +21,14 @@ struct Chunk {
 
 __device__ __forceinline__ void load_row_chunk(const double *p, Chunk<double> &r)
 {
-    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
         : "l"(p));
 }
 
 __device__ __forceinline__ void load_row_chunk(const float *p, Chunk<float> &r)
 {
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
           "=f"(r.v[6]), "=f"(r.v[7])
         : "l"(p));
@@ -60,7 +60,7 @@ __device__ __forceinline__ uint32_t load_id(const uint32_t *p)
 __device__ __forceinline__ uint32_t load_map(const uint32_t *p)
 {
     uint32_t v;
-    asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
@@ -82,20 +82,25 @@ __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, 
 // `id`'s losses.  0: dense row map[id] (one 4-byte L2 read per event); 1: row id of the direct
 // store (no read: the L1 data pipe is the scan's binding resource and the map read was a third
 // of its wavefronts); 2: as 1 behind the shared-memory presence bitmap `sbits`, so absent ids
-// read the one zero row instead of a cold line of the direct store.  Out-of-range ids read the
-// zero row and raise `bad`.
+// read an L2-resident zero row instead of a cold line of the direct store.  Absent and
+// out-of-range ids read a zero row of the zero-row block (ara_internal.h kZeroRows); out-of-range
+// ids also raise `bad`.
 template <int MM>
 __device__ __forceinline__ uint32_t row_index(const uint32_t *__restrict__ map,
                                               const uint32_t *sbits, uint32_t id, uint32_t C,
-                                              bool &bad)
+                                              uint32_t zero_base, bool &bad)
 {
     const bool ok = (id - 1u) < C;  // id in [1, C]
     bad |= !ok;
-    if (MM == 0) return load_map(map + (ok ? id : 0u));  // map[0] == 0: the zero row
-    if (MM == 1) return ok ? id : 0u;
+    const uint32_t z = zero_base + (id & (kZeroRows - 1u));  // a zero row (absent, out of range)
+    if (MM == 0) {
+        const uint32_t r = load_map(map + (ok ? id : 0u));  // map[0] == 0
+        return r ? r : z;
+    }
+    if (MM == 1) return ok ? id : z;
     const uint32_t h = bitmap_hash(id);
     const uint32_t w = sbits[h >> 5];
-    return (ok && ((w >> (h & 31u)) & 1u)) ? id : 0u;
+    return (ok && ((w >> (h & 31u)) & 1u)) ? id : z;
 }
 
 // Mode 2: copy the presence bitmap into this block's shared memory (64 KB, 16-byte loads).
