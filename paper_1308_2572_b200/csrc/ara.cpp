@@ -182,7 +182,7 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
         perm = ctx->sort.perm;
     }
     ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
-                      0u,  // zero_base: set per launch from the store the kernel reads
+                      0u, 0u,  // zero_base, bitmap_log2: set per launch by the kernel's store
                       dyn ? ctx->d_ticket : nullptr,
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
@@ -339,15 +339,18 @@ ara_status build_direct(ara_ctx *ctx)
     e = ara::launch_expand_rows(st.d_map, ctx->C, uni ? (const void *)st.uni.d_rows : st.d_rows,
                                 direct, row_bytes, ctx->stream);
     if (e == cudaSuccess && mode == 2) {
-        e = cudaMalloc(&st.d_bitmap, ara::kBitmapWords * 4);
-        if (e == cudaSuccess) e = ara::launch_build_bitmap(st.d_map, ctx->C, st.d_bitmap, ctx->stream);
+        st.bitmap_log2 = uni ? ara::kBitmapLog2Union : ara::kBitmapLog2Scan;
+        e = cudaMalloc(&st.d_bitmap, ara::bitmap_bytes(st.bitmap_log2));
+        if (e == cudaSuccess)
+            e = ara::launch_build_bitmap(st.d_map, ctx->C, st.d_bitmap, st.bitmap_log2,
+                                         ctx->stream);
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "direct store");
     st.map_mode = mode;
     st.zero_base_direct = ctx->C + 1;
     st.uni.zero_base_direct = ctx->C + 1;
-    ctx->store_bytes += bytes + (mode == 2 ? ara::kBitmapWords * 4 : 0);
+    ctx->store_bytes += bytes + (mode == 2 ? ara::bitmap_bytes(st.bitmap_log2) : 0);
     return ARA_OK;
 }
 

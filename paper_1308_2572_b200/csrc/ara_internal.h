@@ -107,7 +107,8 @@ struct DeviceStore {
     // bitmap held in shared memory (absent ids read the zero row instead of a cold line).
     int map_mode = 0;
     void *d_rows_direct = nullptr;  // [(C+1+kZeroRows) * n_layers * W]: row id = dense map[id]
-    uint32_t *d_bitmap = nullptr;   // [kBitmapWords]: bit h(id) set when map[id] != 0
+    uint32_t *d_bitmap = nullptr;   // [2^bitmap_log2 bits]: bit h(id) set when map[id] != 0
+    uint32_t bitmap_log2 = 0;
     void *d_rows = nullptr;      // [(U+1+kZeroRows) * n_layers * W] double or float; row 0 and
                                  // rows U+1.. (the zero-row block) are zero
     uint32_t zero_base = 0;      // U + 1
@@ -122,15 +123,17 @@ struct DeviceStore {
 // gathers bypass L1, so a single shared zero line would be one hot L2 slice).
 constexpr uint32_t kZeroRows = 1024;
 
-// Presence bitmap of map mode 2: 2^19 bits (64 KB of shared memory per block, three blocks per
-// SM), bit h(id) = Fibonacci hash of the catalogue id.  A clear bit proves the id absent; a set
-// bit may be a collision (then the direct row, all zeros, is read).
-constexpr int kBitmapLog2 = 19;
-constexpr uint32_t kBitmapWords = 1u << (kBitmapLog2 - 5);
-__host__ __device__ inline uint32_t bitmap_hash(uint32_t id)
+// Presence bitmap of map mode 2: 2^b bits, bit h(id) = Fibonacci hash of the catalogue id.  A
+// clear bit proves the id absent; a set bit may be a collision (then the direct row, all zeros,
+// is read).  b = 19 (64 KB of shared memory per block, three blocks per SM) for the scan kernel,
+// b = 18 for the union-row kernel (its blocks also hold their F rows in shared memory).
+constexpr int kBitmapLog2Scan = 19;
+constexpr int kBitmapLog2Union = 18;
+__host__ __device__ inline uint32_t bitmap_hash(uint32_t id, uint32_t log2_bits)
 {
-    return (id * 0x9E3779B1u) >> (32 - kBitmapLog2);
+    return (id * 0x9E3779B1u) >> (32 - log2_bits);
 }
+inline size_t bitmap_bytes(uint32_t log2_bits) { return (size_t)1 << (log2_bits - 3); }
 
 struct ScanLaunch {
     const uint64_t *offsets;  // [n+1], device
@@ -141,6 +144,7 @@ struct ScanLaunch {
     uint32_t catalogue_size;
     uint32_t *err;            // device error word (bit 0: id out of range)
     uint32_t zero_base;       // first row of the zero-row block of the rows the kernel reads
+    uint32_t bitmap_log2;     // map mode 2: log2 of the presence bitmap's bit count
     unsigned long long *counter;  // dynamic ticket counter (NULL: static assignment)
     unsigned int *done;           // finished-block counter (resets `counter`)
     double *max_occ;              // F4: [n_layers][max_occ_ld] or NULL
@@ -165,7 +169,7 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
 cudaError_t launch_expand_rows(const uint32_t *d_map, uint32_t C, const void *dense,
                                void *direct, size_t row_bytes, cudaStream_t stream);
 cudaError_t launch_build_bitmap(const uint32_t *d_map, uint32_t C, uint32_t *bitmap,
-                                cudaStream_t stream);
+                                uint32_t log2_bits, cudaStream_t stream);
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int map_mode,

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                      const UnionTermsDev *__restrict__ ut)
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
-    load_bitmap<MM>(sbits, bitmap);
+    load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
     constexpr int WU = 8 * GU;              // union row width (doubles)
     constexpr int GS = u_row_doubles<GU>(); // shared F row stride per group (doubles)
     constexpr int ZERO = u_slot(WU);        // index of the zero pair
@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     for (int i = 0; i < kUnionMaxE / 2; ++i) slot2[i] = ut->slot2[ly][i];
     double *const ylt_row = s.ylt + (size_t)ly * s.ylt_ld;
     const double *__restrict__ my_rows = urows + 4 * c;
-    const uint32_t C = s.catalogue_size;
     const uint32_t zb = s.zero_base;
+    const RowLookup look{map, sbits, s.catalogue_size, zb, s.bitmap_log2};
     __syncwarp();
 
     // one event: F of this lane's columns -> shared row -> this lane's layer sum and state
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             double S = 0.0, Cprev = 0.0, lr = 0.0;
             while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {  // unaligned head
                 Chunk<double> r[2];
-                gather(row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
+                gather(row_index<MM>(look, load_id(ev), bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                 uint32_t id_c[8], id_n[8];
                 load_ids8(ev, id_c);
                 if (n_chunks > 1) load_ids8(ev + 8, id_n);
-                uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, zb, bad);
+                uint32_t idx1 = row_index<MM>(look, id_c[1], bad);
                 Chunk<double> ra[2];
-                gather(row_index<MM>(map, sbits, id_c[0], C, zb, bad), ra);
+                gather(row_index<MM>(look, id_c[0], bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -161,11 +161,11 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                         const uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                         const uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                         const bool ok2 = j + 2 < 8 || more;
-                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
                         Chunk<double> rb[2];
                         gather(pin(idx1, S), rb);
                         event(ra, S, Cprev, lr);
-                        const uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, zb, bad) : zb;
+                        const uint32_t idx3 = ok2 ? row_index<MM>(look, id3, bad) : zb;
                         gather(pin(idx2, S), ra);
                         event(rb, S, Cprev, lr);
                         idx1 = idx3;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kScanThreads, 3)
             }
             while (ev < ev_end) {  // tail
                 Chunk<double> r[2];
-                gather(row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
+                gather(row_index<MM>(look, load_id(ev), bad), r);
                 event(r, S, Cprev, lr);
                 ++ev;
             }
@@ -215,7 +215,7 @@ template <int GU, bool BAL, int MM>
 cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32_t *d_bitmap,
                        const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
-    const size_t smem = MM == 2 ? kBitmapWords * 4 : 0;
+    const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Union) : 0;
     static int occ = 0;
     if (occ == 0) {
         cudaError_t e = cudaFuncSetAttribute(portfolio_kernel<GU, BAL, MM>,
@@ -236,6 +236,7 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
     if (blocks > max_blocks) blocks = max_blocks;
     ScanLaunch sl = s;
     sl.zero_base = MM ? us.zero_base_direct : us.zero_base;
+    sl.bitmap_log2 = kBitmapLog2Union;
     portfolio_kernel<GU, BAL, MM><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();

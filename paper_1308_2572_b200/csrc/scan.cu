@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                 const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
-    load_bitmap<MM>(sbits, bitmap);
+    load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
     constexpr int PER = Chunk<R>::N;
     constexpr int W = PER * G * CH;  // row width per layer (elements)
     constexpr int NCOL = PER * CH;   // columns per lane
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     const uint64_t groups = ((uint64_t)gridDim.x * blockDim.x) / G;
     const uint32_t leader = lane - c;
     const uint32_t row_stride = n_layers * W;  // elements per union row
-    const uint32_t C = s.catalogue_size;
     const uint32_t zb = s.zero_base;
+    const RowLookup look{map, sbits, s.catalogue_size, zb, s.bitmap_log2};
 
     R rate[NCOL], ret[NCOL], lim[NCOL];  // terms I_j of this lane's columns
     R occ_ret = 0, occ_lim = 0, agg_ret = 0, agg_lim = 0;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                 Chunk<R> ring[D][CH];
 #pragma unroll
                 for (int e = 0; e < D; ++e)
-                    gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, id_c[e], C, zb, bad),
+                    gather<CH, R>(my_rows, row_stride, row_index<MM>(look, id_c[e], bad),
                                   ring[e]);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                         const int e2 = j + D;  // refill: event j + D of this chunk or the next
                         const uint32_t id2 = e2 < 8 ? id_c[e2 < 8 ? e2 : 0] : id_n[e2 < 8 ? 0 : e2 - 8];
                         const bool ok2 = e2 < 8 || more;
-                        const uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
+                        const uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
                         gather<CH, R>(my_rows, row_stride, pin(idx2, S), ring[j % D]);
                     }
 #pragma unroll
@@ -227,8 +227,8 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             uint32_t id_c[8], id_n[8];
             load_ids8(ev, id_c);
             if (n_chunks > 1) load_ids8(ev + 8, id_n);
-            uint32_t idx0 = row_index<MM>(map, sbits, id_c[0], C, zb, bad);
-            uint32_t idx1 = row_index<MM>(map, sbits, id_c[1], C, zb, bad);
+            uint32_t idx0 = row_index<MM>(look, id_c[0], bad);
+            uint32_t idx1 = row_index<MM>(look, id_c[1], bad);
             Chunk<R> ra[CH];
             gather<CH, R>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
@@ -240,13 +240,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     uint32_t id2 = j + 2 < 8 ? id_c[j + 2] : id_n[0];
                     uint32_t id3 = j + 3 < 8 ? id_c[j + 3] : id_n[1];
                     const bool ok2 = j + 2 < 8 || more;
-                    uint32_t idx2 = ok2 ? row_index<MM>(map, sbits, id2, C, zb, bad) : zb;
+                    uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
                     Chunk<R> rb[CH];
                     gather<CH, R>(my_rows, row_stride, pin(idx1, S), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
                     event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
-                    uint32_t idx3 = ok2 ? row_index<MM>(map, sbits, id3, C, zb, bad) : zb;
+                    uint32_t idx3 = ok2 ? row_index<MM>(look, id3, bad) : zb;
                     gather<CH, R>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc);
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         // tail: remaining events one by one
         while (ev < ev_end) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(map, sbits, load_id(ev), C, zb, bad), r);
+            gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -336,7 +336,7 @@ template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D>
 cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                        cudaStream_t stream)
 {
-    const size_t smem = MM == 2 ? kBitmapWords * 4 : 0;
+    const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
     static int occ = 0;  // resident blocks per SM for this instantiation
     if (occ == 0) {
         cudaError_t e = cudaFuncSetAttribute(scan_kernel<G, CH, MINB, X, R, BAL, MM, D>,
@@ -369,6 +369,7 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks > max_blocks) blocks = max_blocks;
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
+    sl.bitmap_log2 = kBitmapLog2Scan;
     scan_kernel<G, CH, MINB, X, R, BAL, MM, D><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const R *)(MM ? st.d_rows_direct : st.d_rows),
         (const LayerTermsT<R> *)st.d_terms, st.n_layers);
@@ -403,12 +404,13 @@ __global__ void expand_rows_kernel(const uint32_t *__restrict__ map, uint32_t C,
     }
 }
 
-__global__ void build_bitmap_kernel(const uint32_t *__restrict__ map, uint32_t C, uint32_t *bits)
+__global__ void build_bitmap_kernel(const uint32_t *__restrict__ map, uint32_t C, uint32_t *bits,
+                                    uint32_t log2_bits)
 {
     for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x + 1; id <= C && id != 0;
          id += gridDim.x * blockDim.x)
         if (map[id]) {
-            const uint32_t h = bitmap_hash(id);
+            const uint32_t h = bitmap_hash(id, log2_bits);
             atomicOr(bits + (h >> 5), 1u << (h & 31u));
         }
 }
@@ -423,11 +425,11 @@ cudaError_t launch_expand_rows(const uint32_t *d_map, uint32_t C, const void *de
 }
 
 cudaError_t launch_build_bitmap(const uint32_t *d_map, uint32_t C, uint32_t *bitmap,
-                                cudaStream_t stream)
+                                uint32_t log2_bits, cudaStream_t stream)
 {
-    cudaError_t e = cudaMemsetAsync(bitmap, 0, kBitmapWords * 4, stream);
+    cudaError_t e = cudaMemsetAsync(bitmap, 0, bitmap_bytes(log2_bits), stream);
     if (e != cudaSuccess) return e;
-    build_bitmap_kernel<<<592, 256, 0, stream>>>(d_map, C, bitmap);
+    build_bitmap_kernel<<<592, 256, 0, stream>>>(d_map, C, bitmap, log2_bits);
     return cudaGetLastError();
 }
 

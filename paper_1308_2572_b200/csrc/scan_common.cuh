@@ -85,32 +85,40 @@ __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, 
 // read an L2-resident zero row instead of a cold line of the direct store.  Absent and
 // out-of-range ids read a zero row of the zero-row block (ara_internal.h kZeroRows); out-of-range
 // ids also raise `bad`.
+struct RowLookup {
+    const uint32_t *__restrict__ map;  // mode 0: catalogue map
+    const uint32_t *sbits;             // mode 2: presence bitmap in shared memory
+    uint32_t C;                        // catalogue size
+    uint32_t zero_base;                // first row of the zero-row block
+    uint32_t bitmap_log2;              // mode 2: log2 of the bitmap's bit count
+};
+
 template <int MM>
-__device__ __forceinline__ uint32_t row_index(const uint32_t *__restrict__ map,
-                                              const uint32_t *sbits, uint32_t id, uint32_t C,
-                                              uint32_t zero_base, bool &bad)
+__device__ __forceinline__ uint32_t row_index(const RowLookup &L, uint32_t id, bool &bad)
 {
-    const bool ok = (id - 1u) < C;  // id in [1, C]
+    const bool ok = (id - 1u) < L.C;  // id in [1, C]
     bad |= !ok;
-    const uint32_t z = zero_base + (id & (kZeroRows - 1u));  // a zero row (absent, out of range)
+    const uint32_t z = L.zero_base + (id & (kZeroRows - 1u));  // a zero row (absent, out of range)
     if (MM == 0) {
-        const uint32_t r = load_map(map + (ok ? id : 0u));  // map[0] == 0
+        const uint32_t r = load_map(L.map + (ok ? id : 0u));  // map[0] == 0
         return r ? r : z;
     }
     if (MM == 1) return ok ? id : z;
-    const uint32_t h = bitmap_hash(id);
-    const uint32_t w = sbits[h >> 5];
+    const uint32_t h = bitmap_hash(id, L.bitmap_log2);
+    const uint32_t w = L.sbits[h >> 5];
     return (ok && ((w >> (h & 31u)) & 1u)) ? id : z;
 }
 
-// Mode 2: copy the presence bitmap into this block's shared memory (64 KB, 16-byte loads).
+// Mode 2: copy the presence bitmap into this block's shared memory (16-byte loads).
 template <int MM>
-__device__ __forceinline__ void load_bitmap(uint32_t *sbits, const uint32_t *__restrict__ bitmap)
+__device__ __forceinline__ void load_bitmap(uint32_t *sbits, const uint32_t *__restrict__ bitmap,
+                                            uint32_t log2_bits)
 {
     if (MM != 2) return;
     const uint4 *src = reinterpret_cast<const uint4 *>(bitmap);
     uint4 *dst = reinterpret_cast<uint4 *>(sbits);
-    for (uint32_t i = threadIdx.x; i < kBitmapWords / 4; i += blockDim.x) dst[i] = src[i];
+    const uint32_t n16 = 1u << (log2_bits - 7);
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     __syncthreads();
 }
 

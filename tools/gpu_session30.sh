@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2 | tee gpurun_out/pytest_gpu_30.txt
+timeout 300 python tools/tune_scan.py --config headline --variants 0:0:2,0:0:1 --reps 5 2>&1 | tee gpurun_out/tune_30.jsonl
+timeout 300 python tools/tune_scan.py --config portfolio --variants 0:0:2,0:0:1,0:0:0 --reps 3 2>&1 | tee -a gpurun_out/tune_30.jsonl
+for c in sweep-e32 sweep-e64; do timeout 300 python tools/tune_scan.py --config $c --variants 0:0:2,8:0:2 --reps 3 2>&1 | tee -a gpurun_out/tune_30.jsonl; done
