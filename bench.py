@@ -8,8 +8,9 @@ A step is one pass of the whole hot path over one batch: 
 scans its contiguous trial slice of the YET (ara_run: A2-A8, device-resident inputs), the YLT
 slices are all-gathered over NCCL (N > 1), and PML/TVaR at the return periods are computed
 (ara_metrics: A9).  The ELT store build (A1, ara_set_layers) is setup and not timed (it is the
-paper's preprocessing stage).  Strong scaling: the 1M-trial workload is split over
-the ranks.  Inputs are synthetic (datagen/, seed 1308) with the paper's workload shape.
+paper's preprocessing stage).  Weak scaling by default (trials are independent
+units): every rank scans its own 1M-trial slice of an N x 1M-trial YET, and
+PML/TVaR are taken over the whole gathered YLT; ``--scaling strong`` splits the 1M trials instead.  Inputs are synthetic (datagen/, seed 1308) with the paper's workload shape.
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on
 the context stream, max over ranks.  The YET (4 GB at the headline) is larger than L2, so every
@@ -179,7 +180,7 @@ def run_reference(args, spec):
     cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_name(spec),
                                             "parallelism": "host threads (oracle)"},
             "cpu_baseline": cb,
@@ -198,6 +199,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the graded fp64 path; 32: the paper's float variant (F3)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: n_trials per rank (N x n in total); strong: n_trials split over ranks")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -236,7 +239,8 @@ def main():
     from paper_1308_2572_b200 import dist as adist
     if world > 1:  # setup collective: rank 0's ELTs and terms reach every rank (NVLink)
         adist.broadcast_inputs(ds, src=0)
-    t0, t1 = partition(spec.n_trials, rank, world)
+    n_total = spec.n_trials * world if args.scaling == "weak" else spec.n_trials
+    t0, t1 = partition(n_total, rank, world)
     n_loc = t1 - t0
     h_off_np = datagen.trial_offsets(spec, t0, n_loc)
     n_ev = int(h_off_np[-1])
@@ -247,7 +251,7 @@ def main():
     d_ids = h_ids.to(dev).view(torch.uint32)
     L = ds.n_layers
     d_ylt_loc = torch.empty((L, n_loc), dtype=torch.float64, device=dev)
-    d_ylt_full = torch.empty((L, spec.n_trials), dtype=torch.float64, device=dev)
+    d_ylt_full = torch.empty((L, n_total), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     ctx = ara.Context(local, stream)
     ctx.ara_set_precision(args.precision)
@@ -263,7 +267,7 @@ def main():
     def gather():
         if world == 1:
             return d_ylt_loc
-        return adist.gather_ylt(d_ylt_loc, spec.n_trials, out=d_ylt_full)
+        return adist.gather_ylt(d_ylt_loc, n_total, out=d_ylt_full)
 
     scan_ev = []
 
@@ -304,7 +308,11 @@ def main():
     if world > 1:
         ms, scan_ms = adist.max_over_ranks([ms, scan_ms])
 
-    trial_events = spec.trial_events * spec.n_layers
+    # every rank's events (weak scaling: N slices of the workload; strong: one split over ranks)
+    n_ev_all = n_ev
+    if world > 1:
+        n_ev_all = int(adist.sum_over_ranks([float(n_ev)])[0])
+    trial_events = n_ev_all * spec.n_layers
     value = trial_events / (ms * 1e-3)
     # roofline of the dominant kernel (the scan): algorithmic bytes per launch (DESIGN.md
     # "Roofline"): per layer n*k*(4 + 8E) + n*8 (YLT) + (n+1)*8 (offsets); per rank.
@@ -370,12 +378,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (datagen SplitMix64, seed 1308; truncated-Pareto ELT losses)",
-            "config": {"workload": workload_name(spec), "layers": L, "elts_per_layer": E,
-                       "trials": spec.n_trials, "events_per_trial": spec.k_min,
-                       "parallelism": f"trial-sharded x{world} (NCCL all-gather of the YLT)"
+            "config": {"workload": workload_name(spec) + (
+                           f" per GPU ({n_total} trials in total)"
+                           if world > 1 and args.scaling == "weak" else ""), "layers": L, "elts_per_layer": E,
+                       "trials": n_total, "trials_per_gpu": n_loc,
+                       "events_per_trial": spec.k_min,
+                       "parallelism": f"trial-sharded x{world}, {args.scaling} scaling "
+                                      f"(NCCL all-gather of the YLT for PML/TVaR)"
                        if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2: the 4 GB YET is streamed from HBM every "
                              "step; the ELT store (2.6 MB rows + 8 MB map) is L2-resident",

@@ -79,8 +79,8 @@ class GenSpec:
     # layer-term multipliers of the scale M = sum_j rate_j * median_j (see layer_terms()):
     occ_ret_m: float = 0.6608
     occ_lim_m: float = 2.9150
-    agg_ret_m: float = 0.4772
-    agg_lim_m: float = 0.0461
+    agg_ret_m: float = 0.4783
+    agg_lim_m: float = 0.0986
 
     def replace(self, **kw) -> "GenSpec":
         return dataclasses.replace(self, **kw)
@@ -91,23 +91,24 @@ class GenSpec:
 
 
 # Aggregate multipliers were calibrated once with scripts/calibrate_terms.py (which runs the
-# oracle on the first 1,000 trials of seed 1308) so that AggR sits near the 30th percentile
-# and AggR + AggL near the 90th percentile of the trial's occurrence-capped sum.
+# oracle on the first 100,000 trials of seed 1308; tiny: all 1,000) so that AggR sits near the 30th percentile
+# and AggR + AggL near the 99.95th percentile (tiny: 99.9th) of the trial's occurrence-capped sum,
+# so PML/TVaR at the return periods 10-1000 years lie below the aggregate limit.
 PRESETS = {
     # BASELINE.json configs[0]
     "tiny": GenSpec("tiny", catalogue_size=1000, pool_size=200, n_elts=2, records_per_elt=100,
                     elts_per_layer=2, n_trials=1000, k_min=10, k_max=10, hit=0.5,
-                    occ_ret_m=0.1823, occ_lim_m=3.9561, agg_ret_m=0.0962, agg_lim_m=0.5284),
+                    occ_ret_m=0.1823, occ_lim_m=3.9561, agg_ret_m=0.0962, agg_lim_m=1.3452),
     # configs[1]
     "medium": GenSpec("medium", n_trials=100_000,
-                      occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4772, agg_lim_m=0.0461),
+                      occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4783, agg_lim_m=0.0986),
     # configs[2] (paper headline: 1 layer, 1,000,000 trials x 1,000 events)
     "headline": GenSpec("headline", n_trials=1_000_000,
-                        occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4772, agg_lim_m=0.0461),
+                        occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4783, agg_lim_m=0.0986),
     # configs[3] multi-layer portfolio: 8 layers sharing 64 ELTs
     "portfolio": GenSpec("portfolio", n_elts=64, n_layers=8, elts_per_layer=16,
                          layer_stride=8, n_trials=1_000_000,
-                         occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4772, agg_lim_m=0.0461),
+                         occ_ret_m=0.6608, occ_lim_m=2.9150, agg_ret_m=0.4783, agg_lim_m=0.0986),
 }
 # configs[4] scaling sweep (F2): events per trial 500-2000 and variable 800-1500,
 # ELTs per layer 4-64, trials up to 8M.  Same generator, multipliers as the headline.

@@ -112,3 +112,12 @@ def max_over_ranks(values: Sequence[float]):
     t = torch.tensor(list(values), dtype=torch.float64, device=_dev_for(dist))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.cpu().tolist()
+
+
+def sum_over_ranks(values: Sequence[float]):
+    """Element-wise sum over ranks (event counts of the rank slices)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(values), dtype=torch.float64, device=_dev_for(dist))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.cpu().tolist()
