@@ -331,11 +331,12 @@ def main():
             pj = json.load(open(prof)).get(spec.name)
             if pj and pj.get("n_trials") == n_loc and args.precision == 64:
                 traffic = pj["dram_bytes_per_launch"]
-                physical = {"bound": "l1_data_pipe (LSU wavefronts)",
-                            "l1_data_pipe_busy": pj["l1_data_pipe_busy"],
-                            "l2_throughput": pj["lts_throughput"],
-                            "dram_bytes_per_launch": traffic,
-                            "source": "ncu capture committed in profiles/ (same kernel, config)"}
+                physical = {k: pj[k] for k in ("bound", "dram_bytes_per_launch", "l2_hit_rate",
+                                                "l1_data_pipe_busy", "lts_throughput",
+                                                "fp64_pipe", "alu_pipe", "issue_active")
+                            if k in pj}
+                physical["source"] = ("ncu capture committed in profiles/ (same kernel and "
+                                      "config; scan_traffic.json)")
         except Exception:
             pass
 

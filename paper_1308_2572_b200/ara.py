@@ -70,11 +70,15 @@ class Info(ctypes.Structure):
 
 
 def _load() -> ctypes.CDLL:
-    if not os.path.exists(LIB_PATH):
+    path = LIB_PATH
+    variant = os.environ.get("ARA_LIB_VARIANT")  # tuning builds: libara_<variant>.so (build.py)
+    if variant:
+        path = os.path.join(_PKG, f"libara_{variant}.so")
+    if not os.path.exists(path):
         raise AraLibraryMissing(
-            f"{LIB_PATH} is not built; run `python -m paper_1308_2572_b200.build` "
+            f"{path} is not built; run `python -m paper_1308_2572_b200.build` "
             "(there is no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     p, u32, u64, i32, d = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
                            ctypes.c_double)
     sig = {

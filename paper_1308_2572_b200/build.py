@@ -48,19 +48,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
+    """Build libara.so; ``variant`` + ``defines`` build a tuning library libara_<variant>.so
+    with extra -D flags (loaded by the binding when ARA_LIB_VARIANT=<variant>)."""
+    lib = LIB if not variant else os.path.join(PKG, f"libara_{variant}.so")
+    if not variant and not force and not _stale():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     objs = []
     for src in _sources():
         name = os.path.basename(src)
-        obj = os.path.join(BUILD, name + ".o")
-        cmd = [NVCC, *ARCH, *COMMON, *PER_FILE[name], "-c", src, "-o", obj]
+        obj = os.path.join(BUILD, (f"{variant}_" if variant else "") + name + ".o")
+        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], *PER_FILE[name], "-c", src,
+               "-o", obj]
         if src.endswith(".cpp"):
-            cmd = [NVCC, *COMMON, "-x", "cu", *ARCH, "-c", src, "-o", obj]
+            cmd = [NVCC, *COMMON, *[f"-D{d}" for d in defines], "-x", "cu", *ARCH, "-c", src,
+                   "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        with open(os.path.join(BUILD, f"ptxas_{name}.txt"), "w") as f:
+        with open(os.path.join(BUILD, f"ptxas_{variant}{name}.txt"), "w") as f:
             f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -68,11 +74,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stdout.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_1308_2572_b200.build [--force] [-v] [--variant NAME -DFOO=1 ...]
+    a = sys.argv[1:]
+    var = a[a.index("--variant") + 1] if "--variant" in a else ""
+    print(build(force="--force" in a, verbose="-v" in a, variant=var,
+                defines=tuple(x[2:] for x in a if x.startswith("-D"))))

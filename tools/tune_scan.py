@@ -75,7 +75,10 @@ def main():
         same = True if ref is None else bool(np.array_equal(out, ref))
         ref = out if ref is None else ref
         ms = float(np.median(ts))
-        print(json.dumps({"variant": v, "env": args.env, "sched": args.sched or f"flags={args.flags}",
+        import hashlib
+        print(json.dumps({"variant": v, "lib": os.environ.get("ARA_LIB_VARIANT", ""),
+                          "ylt_sha1": hashlib.sha1(out.tobytes()).hexdigest()[:16],
+                          "env": args.env, "sched": args.sched or f"flags={args.flags}",
                           "config": args.config, "ms_median": ms,
                           "ms_min": float(min(ts)), "GBps_alg": bytes_alg / ms / 1e6,
                           "trial_events_per_s": n_ev * ds.n_layers / ms * 1e3,
