@@ -246,6 +246,10 @@ typedef struct {
                                     0 = catalogue map -> dense row; 1 = rows indexed by
                                     catalogue id; 2 = as 1 behind a shared-memory presence
                                     bitmap.  Results are identical in every mode.          */
+    int layer_kernel;            /* how several layers are scanned: 0 = rows
+                                    per layer (one fused launch); 1 = union rows, layer sums
+                                    through a shared-memory F row; 2 = union rows, layer sums
+                                    through register shuffles.  Identical results.          */
 } ara_info;
 
 ara_status ara_get_info(const ara_ctx *ctx, ara_info *out);

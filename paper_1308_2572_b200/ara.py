@@ -66,7 +66,7 @@ class Info(ctypes.Structure):
                 ("n_layers", ctypes.c_uint32), ("max_row_width", ctypes.c_uint32),
                 ("store_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("device", ctypes.c_int), ("sm_count", ctypes.c_int),
-                ("row_addressing", ctypes.c_int)]
+                ("row_addressing", ctypes.c_int), ("layer_kernel", ctypes.c_int)]
 
 
 def _load() -> ctypes.CDLL:

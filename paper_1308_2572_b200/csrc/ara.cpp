@@ -261,6 +261,37 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     if (GU > 8) return ARA_OK;
     const uint32_t WU = 8 * GU;
     auto u_slot = [](uint32_t col) { return col + 2 * (col >> 3); };
+    // Register-shuffle layout (portfolio.cu): every ELT must sit in register (i mod 8) of some
+    // lane for each position i it takes in a layer, so that one shuffle per position serves
+    // every layer of the group; at most GU ELTs per register.  When the layer lists allow it
+    // (configuration P does: ELT e is at positions e mod 8 and 8 + e mod 8), union column
+    // `col` moves to lane lane_of[col], register reg_of[col]; otherwise the shared-memory F row
+    // serves the layer sums.
+    std::vector<int> reg_of(J.size(), -1), lane_of(J.size(), -1);
+    bool shfl = true;
+    for (uint32_t l = 0; l < L && shfl; ++l)
+        for (uint32_t c = elt_offsets[l]; c < elt_offsets[l + 1]; ++c) {
+            const int col = col_of[elt_index[c]], r = (int)((c - elt_offsets[l]) % 8);
+            if (reg_of[col] >= 0 && reg_of[col] != r) shfl = false;
+            reg_of[col] = r;
+        }
+    if (shfl) {
+        std::vector<int> used(8, 0);
+        for (size_t col = 0; col < J.size() && shfl; ++col) {
+            lane_of[col] = used[reg_of[col]]++;
+            if (lane_of[col] >= (int)GU) shfl = false;
+        }
+    }
+    if (GU != 8) shfl = false;  // shuffle variants are built for GU = 8 only (portfolio.cu)
+    if (const char *e = getenv("ARA_PORTFOLIO_SHFL"))
+        if (atoi(e) == 0) shfl = false;
+    // the union column that holds J[col]: lane c's registers 0-3 are columns 4c..4c+3 and
+    // registers 4-7 are columns 4(c+GU)..4(c+GU)+3 (portfolio.cu, the two gathers of a group)
+    auto ucol = [&](uint32_t col) -> uint32_t {
+        if (!shfl) return col;
+        const uint32_t r = (uint32_t)reg_of[col], c = (uint32_t)lane_of[col];
+        return r < 4 ? 4 * c + r : 4 * (c + GU) + (r - 4);
+    };
     std::vector<double> rows((size_t)(st.n_union + 1 + ara::kZeroRows) * WU, 0.0);
     ara::UnionTermsDev ut{};
     for (uint32_t col = 0; col < WU; ++col) {  // padding columns: neutral terms, zero losses
@@ -269,14 +300,23 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
         ut.lim[col] = INFINITY;
     }
     for (uint32_t col = 0; col < J.size(); ++col) {
-        const uint32_t j = J[col];
+        const uint32_t j = J[col], u = ucol(col);
         for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)  // bit copies
-            rows[(size_t)map[ctx->rec_ids[r]] * WU + col] = ctx->rec_losses[r];
-        ut.rate[col] = ctx->fin[j].rate;
-        ut.ret[col] = ctx->fin[j].retention;
-        ut.lim[col] = ctx->fin[j].limit;
+            rows[(size_t)map[ctx->rec_ids[r]] * WU + u] = ctx->rec_losses[r];
+        ut.rate[u] = ctx->fin[j].rate;
+        ut.ret[u] = ctx->fin[j].retention;
+        ut.lim[u] = ctx->fin[j].limit;
     }
     ut.n_layers = L;
+    bool full16 = true;
+    for (uint32_t l = 0; l < L; ++l) {
+        ut.n_cols[l] = st.n_cols[l];
+        full16 = full16 && st.n_cols[l] == (uint32_t)ara::kUnionMaxE;
+        for (uint32_t i = 0; shfl && i < st.n_cols[l]; ++i) {
+            const uint32_t lane = (uint32_t)lane_of[col_of[elt_index[elt_offsets[l] + i]]];
+            ut.src5[l][i / 6] |= lane << (5 * (i % 6));
+        }
+    }
     for (uint32_t l = 0; l < (uint32_t)ara::kUnionMaxLayers; ++l) {
         const bool real = l < L;
         ut.occ_ret[l] = real ? terms[l].occ_retention : 0.0;
@@ -286,12 +326,13 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
         for (uint32_t i = 0; i < (uint32_t)ara::kUnionMaxE; ++i) {
             // layer order = summation order; past the layer's ELTs: the zero slot (+0 neutral)
             uint32_t slot = u_slot(WU);
-            if (real && i < st.n_cols[l]) slot = u_slot(col_of[elt_index[elt_offsets[l] + i]]);
+            if (real && i < st.n_cols[l]) slot = u_slot(ucol(col_of[elt_index[elt_offsets[l] + i]]));
             ut.slot2[l][i / 2] |= slot << (16 * (i % 2));
         }
     }
     ara::UnionStore &us = st.uni;
     us.GU = GU;
+    us.shfl = shfl ? (full16 ? 2 : 1) : 0;
     us.n_cols = (uint32_t)J.size();
     us.zero_base = st.n_union + 1;
     const size_t row_bytes = rows.size() * 8;
@@ -821,6 +862,8 @@ ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
     out->device = ctx->device;
     out->sm_count = ctx->sm_count;
     out->row_addressing = ctx->have_layers ? ctx->store.map_mode : 0;
+    out->layer_kernel = !ctx->have_layers || !ctx->store.uni.enabled ? 0
+                        : 1 + (ctx->store.uni.shfl != 0);
     return ARA_OK;
 }
 

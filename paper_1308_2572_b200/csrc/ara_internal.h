@@ -77,6 +77,11 @@ struct UnionTermsDev {
     double agg_ret[kUnionMaxLayers], agg_lim[kUnionMaxLayers];
     uint32_t slot2[kUnionMaxLayers][kUnionMaxE / 2];  // packed 16-bit shared-memory F slots
     uint32_t n_layers;
+    // register-shuffle layout (portfolio.cu, shfl != 0): the F value of a layer's i-th ELT sits
+    // in register i mod 8 of lane src(l, i) of the group; src5 packs the 16 source lanes of a
+    // layer as 5-bit fields, six per word
+    uint32_t src5[kUnionMaxLayers][3];
+    uint32_t n_cols[kUnionMaxLayers];    // ELTs of each layer
 };
 struct UnionStore {
     bool enabled = false;
@@ -84,6 +89,8 @@ struct UnionStore {
     uint32_t zero_base = 0;              // U + 1: zero-row block of d_rows
     uint32_t zero_base_direct = 0;       // C + 1: zero-row block of d_rows_direct
     uint32_t GU = 0;         // lanes per trial (2, 4 or 8); union row width WU = 8 * GU doubles
+    int shfl = 0;            // layer sums: 0 = shared-memory F row; 1 = register shuffles
+                             // (general); 2 = register shuffles, every layer has 16 ELTs
     uint32_t n_cols = 0;     // |J|
     double *d_rows = nullptr;            // [(U+1+kZeroRows) * WU]
     UnionTermsDev *d_terms = nullptr;

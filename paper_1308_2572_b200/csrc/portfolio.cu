@@ -16,6 +16,13 @@
 // sums layer l's columns in layer order, ((0 + F_{c_l0}) + F_{c_l1}) + ..., exactly the oracle's
 // sequence, and carries layer l's running state.  Padding entries of a layer's column list point
 // at a zero slot (+0 is exactly neutral, reading R12).
+//
+// Register-shuffle variant (SH = 1, 2; UnionStore::shfl): when every ELT takes positions of one
+// residue mod 8 in all layers that hold it (configuration P), ara_set_layers places the ELT of
+// residue r in register r of some lane, so position i of EVERY layer is register i mod 8 of a
+// lane src(l, i): each position is one 64-bit shuffle per group, with no shared-memory writes,
+// reads or barriers (the shared F row cost 2 L1 wavefronts per trial-layer-event, the shuffles
+// cost 1).  SH = 2: every layer has 16 ELTs; SH = 1: shorter layers add +0 past their end.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,7 +43,7 @@ __host__ __device__ constexpr int u_row_doubles()
     return (u_slot(8 * GU) + 2 + 15) / 16 * 16 + 1;
 }
 
-template <int GU, bool BAL, int MM>
+template <int GU, bool BAL, int MM, int SH>
 __global__ void __launch_bounds__(kScanThreads, 3)
     portfolio_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                      const uint32_t *__restrict__ bitmap, const double *__restrict__ urows,
@@ -47,14 +54,14 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     constexpr int WU = 8 * GU;              // union row width (doubles)
     constexpr int GS = u_row_doubles<GU>(); // shared F row stride per group (doubles)
     constexpr int ZERO = u_slot(WU);        // index of the zero pair
-    __shared__ double sF[(kScanThreads / GU) * GS];
+    __shared__ double sF[SH == 0 ? (kScanThreads / GU) * GS : 2];
 
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % GU;
     const uint32_t gmask = (GU == 32) ? 0xffffffffu : (((1u << GU) - 1u) << (lane - c));
     const uint32_t gb = threadIdx.x / GU;   // group index in the block
     double *const myF = sF + gb * GS;
-    if (c == 0) {
+    if (SH == 0 && c == 0) {
         myF[ZERO] = 0.0;
         myF[ZERO + 1] = 0.0;
     }
@@ -76,9 +83,19 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     const uint32_t ly = has_layer ? c : 0;
     const double occ_ret = ut->occ_ret[ly], occ_lim = ut->occ_lim[ly];
     const double agg_ret = ut->agg_ret[ly], agg_lim = ut->agg_lim[ly];
-    uint32_t slot2[kUnionMaxE / 2];  // two 16-bit slots per register
+    uint32_t slot2[SH == 0 ? kUnionMaxE / 2 : 1];  // two 16-bit slots per register
+    if constexpr (SH == 0) {
 #pragma unroll
-    for (int i = 0; i < kUnionMaxE / 2; ++i) slot2[i] = ut->slot2[ly][i];
+        for (int i = 0; i < kUnionMaxE / 2; ++i) slot2[i] = ut->slot2[ly][i];
+    }
+    // register-shuffle layout: source lane of each position (5-bit fields; shfl uses bits 4:0)
+    uint32_t src5[3] = {0, 0, 0};
+    uint32_t my_n = 0;
+    if constexpr (SH != 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) src5[i] = ut->src5[ly][i];
+        my_n = has_layer ? ut->n_cols[ly] : 0;
+    }
     double *const ylt_row = s.ylt + (size_t)ly * s.ylt_ld;
     const double *__restrict__ my_rows = urows + 4 * c;
     const uint32_t zb = s.zero_base;
@@ -96,19 +113,31 @@ __global__ void __launch_bounds__(kScanThreads, 3)
                 const double l = rsub(rmul(r[h].v[q], rate[j]), ret[j]);  // line 9
                 f[j] = dmin(dmax0(l), lim[j]);
             }
-        __syncwarp(gmask);  // the previous event's reads of the shared row are done
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            double *dst = myF + u_slot(4 * (c + GU * h));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) dst[q] = f[4 * h + q];
-        }
-        __syncwarp(gmask);
         double lo = 0.0;  // lines 11-13 for this lane's layer, in the layer's ELT order
+        if constexpr (SH == 0) {
+            __syncwarp(gmask);  // the previous event's reads of the shared row are done
 #pragma unroll
-        for (int i = 0; i < kUnionMaxE; ++i) {
-            const uint32_t sl = (slot2[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-            lo = radd(lo, myF[sl]);
+            for (int h = 0; h < 2; ++h) {
+                double *dst = myF + u_slot(4 * (c + GU * h));
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dst[q] = f[4 * h + q];
+            }
+            __syncwarp(gmask);
+#pragma unroll
+            for (int i = 0; i < kUnionMaxE; ++i) {
+                const uint32_t sl = (slot2[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+                lo = radd(lo, myF[sl]);
+            }
+        } else {
+            // position i of every layer lives in register i mod 8 (of lane src(l, i)): one
+            // 64-bit shuffle per position serves all layers of the group, no shared memory
+#pragma unroll
+            for (int i = 0; i < kUnionMaxE; ++i) {
+                const uint32_t sl = src5[i / 6] >> (5 * (i % 6));
+                double v = __shfl_sync(gmask, f[i % 8], sl, GU);
+                if (SH == 1) v = (uint32_t)i < my_n ? v : 0.0;  // past the layer's ELTs: +0
+                lo = radd(lo, v);
+            }
         }
         const double oc = dmin(dmax0(rsub(lo, occ_ret)), occ_lim);  // line 16
         S = radd(S, oc);                                              // line 19
@@ -211,18 +240,18 @@ __global__ void __launch_bounds__(kScanThreads, 3)
     }
 }
 
-template <int GU, bool BAL, int MM>
+template <int GU, bool BAL, int MM, int SH>
 cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32_t *d_bitmap,
                        const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Union) : 0;
     static int occ = 0;
     if (occ == 0) {
-        cudaError_t e = cudaFuncSetAttribute(portfolio_kernel<GU, BAL, MM>,
+        cudaError_t e = cudaFuncSetAttribute(portfolio_kernel<GU, BAL, MM, SH>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, portfolio_kernel<GU, BAL, MM>,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, portfolio_kernel<GU, BAL, MM, SH>,
                                                           kScanThreads, smem);
         if (e != cudaSuccess) return e;
         if (occ < 1) occ = 1;
@@ -237,19 +266,35 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
     ScanLaunch sl = s;
     sl.zero_base = MM ? us.zero_base_direct : us.zero_base;
     sl.bitmap_log2 = kBitmapLog2Union;
-    portfolio_kernel<GU, BAL, MM><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
+    portfolio_kernel<GU, BAL, MM, SH><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();
 }
 
+template <int GU, bool BAL, int SH>
+cudaError_t launch_pus(const UnionStore &us, const uint32_t *d_map, int map_mode,
+                       const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
+                       cudaStream_t stream)
+{
+    if (map_mode == 1) return launch_pum<GU, BAL, 1, SH>(us, d_map, d_bitmap, s, sm_count, stream);
+    if (map_mode == 2) return launch_pum<GU, BAL, 2, SH>(us, d_map, d_bitmap, s, sm_count, stream);
+    return launch_pum<GU, BAL, 0, SH>(us, d_map, d_bitmap, s, sm_count, stream);
+}
+
+// Layer-sum variant (UnionStore::shfl); the shuffle variants are built for GU = 8 (up to 64
+// union columns and 8 layers, configuration P), smaller unions use the shared-memory F row.
 template <int GU, bool BAL>
 cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, int map_mode,
                       const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
 {
-    if (map_mode == 1) return launch_pum<GU, BAL, 1>(us, d_map, d_bitmap, s, sm_count, stream);
-    if (map_mode == 2) return launch_pum<GU, BAL, 2>(us, d_map, d_bitmap, s, sm_count, stream);
-    return launch_pum<GU, BAL, 0>(us, d_map, d_bitmap, s, sm_count, stream);
+    if constexpr (GU == 8) {
+        if (us.shfl == 2)
+            return launch_pus<GU, BAL, 2>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        if (us.shfl == 1)
+            return launch_pus<GU, BAL, 1>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+    }
+    return launch_pus<GU, BAL, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
 }
 
 }  // namespace

@@ -224,6 +224,49 @@ def test_row_addressing_modes(stream, monkeypatch, mode, preset, kw):
     ctx.close()
 
 
+# --------------------------------------------------------------------------- F1 layer sums
+def _portfolio_variant(kind):
+    """Portfolios of 8 layers over 64 ELTs: 'P' (configuration P: 16 ELTs per layer, ELT e at
+    positions e mod 8 and 8 + e mod 8 -> register-shuffle layout, all layers full), 'ragged'
+    (the same structure with 9-16 ELTs per layer -> shuffle layout with zero padding), 'mixed'
+    (layer lists permuted, so an ELT sits at positions of different residues mod 8 -> no shuffle
+    layout, shared-memory F row)."""
+    spec = datagen.PRESETS["portfolio"].replace(n_trials=700, k_min=0, k_max=90, seed=17)
+    ds = datagen.generate(spec)
+    if kind == "P":
+        return ds, 2
+    rng = np.random.default_rng(3)
+    members = []
+    for l in range(8):
+        m = [(8 * l + i) % 64 for i in range(16)]
+        if kind == "ragged":
+            m = m[: 9 + (l % 8)]
+        else:
+            rng.shuffle(m)
+        members.append(m)
+    ds.elt_offsets = np.cumsum([0] + [len(m) for m in members]).astype(np.uint32)
+    ds.elt_index = np.concatenate([np.array(m, np.uint32) for m in members])
+    return ds, 2 if kind == "ragged" else 1
+
+
+@pytest.mark.parametrize("kind", ["P", "ragged", "mixed"])
+@pytest.mark.parametrize("shfl_env", [None, "0"])
+def test_portfolio_layer_sum_variants(stream, monkeypatch, kind, shfl_env):
+    """The union-row kernel's two ways of forming each layer's ordered ELT sum -- register
+    shuffles (when every ELT has one register residue across the layers that hold it) and the
+    shared-memory F row (always possible; forced with ARA_PORTFOLIO_SHFL=0) -- both give the
+    oracle's YLT bit for bit, including layers shorter than 16 ELTs (+0 padding)."""
+    if shfl_env is not None:
+        monkeypatch.setenv("ARA_PORTFOLIO_SHFL", shfl_env)
+    ds, expect = _portfolio_variant(kind)
+    want = oracle.run_analysis(ds, n_threads=8)
+    ctx = make_ctx(types_ns(ds), stream)
+    assert ctx.ara_get_info().layer_kernel == (1 if shfl_env == "0" else expect)
+    assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx), want)
+    assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
+    ctx.close()
+
+
 # --------------------------------------------------------------------------- store (A1)
 @pytest.mark.parametrize("preset", ["tiny", "medium"])
 def test_store_round_trip(stream, preset):
@@ -499,3 +542,56 @@ def test_f32_error_distribution_vs_f64(stream):
     ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
     assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx)[0:1], y64[None, :])
     ctx.close()
+
+
+# --------------------------------------------------------------------------- full size, sampled
+def _sampled_oracle(spec, ds, sel):
+    """Oracle YLT of the selected trials only: each trial is regenerated alone (the generator is
+    counter-based, so trial t alone equals trial t inside the whole YET) and the oracle runs on
+    that small YET."""
+    offs, evs = [np.zeros(1, np.uint64)], []
+    total = 0
+    for t in sel:
+        o, e = datagen.generate_yet(spec, ds.pool, int(t), 1, n_threads=1)
+        total += int(o[-1])
+        offs.append(np.array([total], np.uint64))
+        evs.append(e.copy())
+    to = np.concatenate(offs)
+    ev = np.concatenate(evs) if evs else np.zeros(0, np.uint32)
+    return oracle.run_analysis(ds, n_threads=8, trial_offsets=to, events=ev)
+
+
+@pytest.mark.parametrize("preset", ["portfolio", "sweep-e4", "sweep-e64", "sweep-k2000",
+                                    "sweep-ragged", "sweep-h10", "sweep-n8m"])
+def test_full_size_config_sampled(stream, preset):
+    """BASELINE.json configs[3] (8-layer portfolio, 1M x 1000) and the configs[4] sweep extremes
+    (E = 4 and 64, k = 2000, k in 800-1500, 10% hit rate, 8M trials = 32 GB of ids) at full
+    size, in the launch configuration bench.py times (default flags): the YET is generated
+    slice by slice straight into device memory; 1,000 sampled trials plus the first and last
+    are bit-identical to the oracle, and 0 <= lr <= AggL holds for every entry."""
+    spec = datagen.PRESETS[preset]
+    ds = datagen.generate(spec, with_yet=False)
+    n = spec.n_trials
+    off = datagen.trial_offsets(spec, 0, n)
+    d_ids = torch.empty(int(off[-1]), dtype=torch.int32, device=DEV)
+    slab = 1_000_000
+    for t0 in range(0, n, slab):
+        m = min(slab, n - t0)
+        o, e = datagen.generate_yet(spec, ds.pool, t0, m)
+        a = int(off[t0])
+        d_ids[a:a + e.shape[0]].copy_(torch.from_numpy(e.view(np.int32)))
+    ctx = make_ctx(ds, stream)
+    ylt = torch.full((ds.n_layers, n), float("nan"), dtype=torch.float64, device=DEV)
+    ctx.ara_run(to_dev(off, "u64"), d_ids.view(torch.uint32), ylt)
+    ctx.ara_synchronize()
+    got = ylt.cpu().numpy()
+    ctx.close()
+    del d_ids
+    torch.cuda.empty_cache()
+    assert not np.isnan(got).any()
+    aggL = ds.layer_terms[:, 3][:, None]
+    assert (got >= 0).all() and (got <= aggL).all()
+    rng = np.random.default_rng(2572)
+    sel = np.concatenate([[0, n - 1], rng.choice(n, 1000, replace=False)]).astype(np.int64)
+    want = _sampled_oracle(spec, ds, sel)
+    assert_bit_identical(got[:, sel], want)
