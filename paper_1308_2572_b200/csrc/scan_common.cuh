@@ -69,6 +69,14 @@ template <typename R>
 __device__ __forceinline__ R dmin(R x, R y) { return (y < x) ? y : x; }
 template <typename R>
 __device__ __forceinline__ R dmax0(R x) { return (x < R(0)) ? R(0) : x; }
+// fp32 (F3): one FMNMX instead of FSETP + FSEL.  Equal to the compare-select for every non-NaN
+// operand pair except a +0/-0 tie, where the sign of a zero may differ; a zero's sign never
+// changes a sum on the scan path (reading R12), so the YLT is unchanged.  (sm_100a has
+// no fp64 min/max instruction: the fp64 path keeps the compare-select.)
+template <>
+__device__ __forceinline__ float dmin<float>(float x, float y) { return fminf(x, y); }
+template <>
+__device__ __forceinline__ float dmax0<float>(float x) { return fmaxf(x, 0.0f); }
 
 __device__ __forceinline__ uint32_t map_index(const uint32_t *__restrict__ map, uint32_t id,
                                               uint32_t C, bool &bad)

@@ -67,3 +67,25 @@ def test_binding_refuses_missing_library(monkeypatch, tmp_path):
     monkeypatch.setattr(ara, "_lib", None)
     with pytest.raises(ara.AraLibraryMissing):
         ara.lib()
+
+
+@pytest.mark.parametrize("cname,pyname", [("ara_fin_terms", "FinTerms"),
+                                          ("ara_layer_terms", "LayerTerms"),
+                                          ("ara_outputs", "Outputs"), ("ara_info", "Info")])
+def test_binding_structs_match_header_layout(tmp_path, cname, pyname):
+    """Every struct the binding passes across the ABI has the header's size and field offsets
+    (compiled with the host C compiler from include/ara.h)."""
+    import subprocess
+    st = getattr(ara, pyname)
+    fields = [f for f, _ in st._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stddef.h>\n#include <stdio.h>\n#include \"ara.h\"\nint main(void){\n"
+                   f"  printf(\"%zu\\n\", sizeof({cname}));\n"
+                   + "".join(f"  printf(\"%zu\\n\", offsetof({cname}, {f}));\n" for f in fields)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src),
+                           "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)], text=True).split()]
+    assert got[0] == ctypes.sizeof(st)
+    assert got[1:] == [getattr(st, f).offset for f in fields]
