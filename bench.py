@@ -201,6 +201,10 @@ def main():
                     help="64: the graded fp64 path; 32: the paper's float variant (F3)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: n_trials per rank (N x n in total); strong: n_trials split over ranks")
+    ap.add_argument("--hoist", action="store_true",
+                    help="ARA_RUN_HOIST: Alg. 1 lines 4-17 once per distinct event per run, then "
+                         "one table read per occurrence (SURVEY.md 7 deferred exact lever; "
+                         "reported separately from the full per-occurrence scan)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -270,12 +274,13 @@ def main():
         return adist.gather_ylt(d_ylt_loc, n_total, out=d_ylt_full)
 
     scan_ev = []
+    run_flags = ara.ARA_RUN_HOIST if args.hoist else 0
 
     def step(timed: bool):
         if timed:
             a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        ctx.ara_run(d_off, d_ids, d_ylt_loc)  # A2-A8: one scan launch per layer
+        ctx.ara_run(d_off, d_ids, d_ylt_loc, flags=run_flags)  # A2-A8: one fused scan launch
         if timed:
             b.record(stream)
             scan_ev.append((a, b))
@@ -321,6 +326,17 @@ def main():
     # E-wide fp64 row segment is gathered per event, every layer's YLT entry is written
     vb = args.precision // 8  # bytes per stored loss
     bytes_alg = n_ev * (4 + vb * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
+    bytes_model = (f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
+                   "segment per event, YLT, offsets (north-star accounting)")
+    if args.hoist:  # what the hoisted pass moves: ids, one value per (occurrence, layer), the
+        # per-event table build (U rows of L*E losses read, U*L values written), YLT, offsets
+        U = ctx.ara_layer_store_shape(0)[0]
+        bytes_alg = (n_ev * (4 + vb * L) + U * L * (vb * E + vb) + 8 * n_loc * L
+                     + 8 * (n_loc + 1))
+        bytes_model = (f"n*k*(4 + {vb}*L) + U*L*({vb}*E + {vb}) + 8*n*L + 8*(n+1): ids, one "
+                       "per-event layer loss per (occurrence, layer), the per-event table build, "
+                       "YLT, offsets (hoisted-scan accounting; not comparable with the "
+                       "north-star bytes of the full scan)")
     peak, peak_src = measured_peak()
     achieved = bytes_alg / (scan_ms * 1e-3) / 1e9
     traffic = None
@@ -328,7 +344,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof)).get(spec.name)
+            pj = json.load(open(prof)).get(spec.name + ("+hoist" if args.hoist else ""))
             if pj and pj.get("n_trials") == n_loc and args.precision == 64:
                 traffic = pj["dram_bytes_per_launch"]
                 physical = {k: pj[k] for k in ("bound", "dram_bytes_per_launch", "l2_hit_rate",
@@ -346,14 +362,14 @@ def main():
         h_ylt = np.empty((L, n_loc))
         ids_np = h_ids.numpy().view(np.uint32)
         for _ in range(2):
-            ctx.ara_run_host(h_off_np, ids_np, h_ylt)
+            ctx.ara_run_host(h_off_np, ids_np, h_ylt, flags=run_flags)
         ts = []
         for _ in range(args.e2e_steps):
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             tt = time.perf_counter()
-            ctx.ara_run_host(h_off_np, ids_np, h_ylt)  # H2D YET, scan, D2H YLT
+            ctx.ara_run_host(h_off_np, ids_np, h_ylt, flags=run_flags)  # H2D YET, scan, D2H YLT
             d_ylt_loc.copy_(torch.from_numpy(h_ylt), non_blocking=False)
             full = gather()
             for l in range(L):
@@ -382,7 +398,10 @@ def main():
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic (datagen SplitMix64, seed 1308; truncated-Pareto ELT losses)",
-            "config": {"workload": workload_name(spec) + (
+            "config": {"variant": ("hoisted (ARA_RUN_HOIST: per-event layer losses once per "
+                                   "distinct event per run; SURVEY.md 7 deferred exact lever)"
+                                   if args.hoist else "full per-occurrence scan (north star)"),
+                       "workload": workload_name(spec) + (
                            f" per GPU ({n_total} trials in total)"
                            if world > 1 and args.scaling == "weak" else ""), "layers": L, "elts_per_layer": E,
                        "trials": n_total, "trials_per_gpu": n_loc,
@@ -395,11 +414,12 @@ def main():
                        "return_periods": list(RETURN_PERIODS)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})",
+                         "kernel": ("hoisted_scan_kernel + hoist_oc_kernel (ara_run, ARA_RUN_HOIST)"
+                                    if args.hoist else
+                                    f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})"),
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
-                         "bytes_model": f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
-                                        "segment per event, YLT, offsets (north-star accounting)",
+                         "bytes_model": bytes_model,
                          "physical": physical},
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -87,6 +87,15 @@ typedef struct {
                                the thread groups of a warp run trials of nearly equal length.
                                This is the default schedule; the flag is accepted for clarity.
                                Results are identical under any schedule.                     */
+#define ARA_RUN_HOIST 8u    /* hoisted scan (deferred exact lever): Alg. 1
+                               lines 4-17 depend only on (event, layer), so each run first
+                               evaluates them once per distinct event of the layers' union
+                               (same fp ops, same order) into a per-event table, then scans
+                               the trials reading one value per (occurrence, layer) for lines
+                               18-29.  The YLT is bit-identical to the full scan.  Up to 8
+                               layers (else ARA_ERR_UNSUPPORTED); ignored by ara_run_outputs
+                               when per-event outputs are requested.  Reported separately
+                               from the full per-occurrence scan (bench.py --hoist).          */
 
 /* Human-readable name of a status code (static storage). */
 const char *ara_status_string(ara_status s);
@@ -162,7 +171,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
  *   d_event_ids[]             device, u32 catalogue ids in [1, C]
  *   d_ylt                     device, fp64, YLT[l][t] at d_ylt[l * ylt_ld + t]
  *   ylt_ld                    row stride of the YLT in elements (0 means n_trials)
- *   flags                     ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE
+ *   flags                     ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE | ARA_RUN_HOIST
  * Without ARA_RUN_SYNC the call only enqueues work on the context stream and returns ARA_OK;
  * an event id outside [1, C] then reads the zero row (never out of bounds) and sets a device
  * error flag that the next ara_synchronize() (or synchronous call) reports as ARA_ERR_RANGE.

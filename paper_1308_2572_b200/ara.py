@@ -23,6 +23,7 @@ STATUS_NAMES = {0: "ARA_OK", 1: "ARA_ERR_ARG", 2: "ARA_ERR_RANGE", 3: "ARA_ERR_V
 ARA_RUN_SYNC = 1
 ARA_RUN_VALIDATE = 2
 ARA_RUN_BALANCE = 4
+ARA_RUN_HOIST = 8
 ARA_MAX_ELTS_PER_LAYER = 64
 ARA_MAX_P = 32
 

@@ -29,6 +29,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-fno-fast-m
 PER_FILE = {
     "scan.cu": ["-fmad=false", "-Xptxas", "-v"],
     "portfolio.cu": ["-fmad=false", "-Xptxas", "-v"],
+    "hoist.cu": ["-fmad=false", "-Xptxas", "-v"],
     "metrics.cu": ["-Xptxas", "-v"],
     "ara.cpp": [],
 }

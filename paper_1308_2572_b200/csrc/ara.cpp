@@ -114,6 +114,9 @@ void free_layers(ara_ctx *ctx)
     cudaFree(ctx->store.uni.d_rows_direct);
     cudaFree(ctx->store.d_rows_direct);
     cudaFree(ctx->store.d_bitmap);
+    cudaFree(ctx->store.d_union_ids);
+    cudaFree(ctx->store.d_oc);
+    cudaFree(ctx->store.d_oc_bitmap);
     ctx->store = ara::DeviceStore();
     ctx->store_bytes = 0;
     ctx->have_layers = false;
@@ -163,6 +166,42 @@ ara_status check_device_error(ara_ctx *ctx)
 
 // One scan launch covers every layer (layer-fused pass: one id read and one map lookup per
 // event serve all layers).
+// ARA_RUN_HOIST (hoist.cu): the per-event layer-loss table, allocated (zeroed) on first use.
+ara_status prepare_hoist(ara_ctx *ctx)
+{
+    ara::DeviceStore &st = ctx->store;
+    if (st.n_layers > 8)
+        return fail(ctx, ARA_ERR_UNSUPPORTED, "ARA_RUN_HOIST supports up to 8 layers (%u)",
+                    st.n_layers);
+    if (!st.d_oc) {
+        uint32_t lp = 1;
+        while (lp < st.n_layers) lp *= 2;
+        const size_t rb = (size_t)lp * (st.bits / 8);
+        int direct = st.map_mode >= 1;
+        size_t bytes = ((size_t)(direct ? ctx->C : st.n_union) + 1) * rb;
+        size_t free_b = 0, total_b = 0;
+        if (direct && (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || bytes > free_b / 4)) {
+            direct = 0;
+            bytes = ((size_t)st.n_union + 1) * rb;
+        }
+        ARA_CUDA(ctx, cudaMalloc(&st.d_oc, bytes));
+        ARA_CUDA(ctx, cudaMemsetAsync(st.d_oc, 0, bytes, ctx->stream));
+        st.oc_lp = lp;
+        st.oc_direct = direct;
+        ctx->store_bytes += bytes;
+        if (direct && st.map_mode == 2) {
+            const size_t bb = ara::bitmap_bytes(ara::kBitmapLog2Hoist);
+            ARA_CUDA(ctx, cudaMalloc(&st.d_oc_bitmap, bb));
+            ARA_CUDA(ctx, ara::launch_build_bitmap(st.d_map, ctx->C, st.d_oc_bitmap,
+                                                   ara::kBitmapLog2Hoist, ctx->stream));
+            ctx->store_bytes += bb;
+        }
+    }
+    cudaError_t e = ara::launch_hoist_oc(st, ctx->stream, &ctx->launches);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hoist kernel launch");
+    return ARA_OK;
+}
+
 ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const uint32_t *d_ids,
                          double *d_ylt, uint64_t ld, uint32_t flags,
                          const ara_outputs *extra = nullptr)
@@ -187,8 +226,11 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
                       extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm};
+    const bool hoist = (flags & ARA_RUN_HOIST) && !extra;
     cudaError_t e =
-        (ctx->store.uni.enabled && !extra)
+        hoist ? ara::launch_hoisted_scan(ctx->store, s, ctx->sm_count, ctx->stream,
+                                         &ctx->launches)
+        : (ctx->store.uni.enabled && !extra)
             ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, ctx->store.map_mode,
                                     ctx->store.d_bitmap, s, ctx->sm_count, ctx->stream,
                                     &ctx->launches)
@@ -642,6 +684,11 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
             e = cudaMemcpy(st.d_rows, rows_buf.data(), row_bytes, cudaMemcpyHostToDevice);
         if (e == cudaSuccess)
             e = cudaMemcpy(st.d_terms, terms_buf.data(), term_bytes, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && st.n_union)
+            e = cudaMalloc(&st.d_union_ids, (size_t)st.n_union * 4);
+        if (e == cudaSuccess && st.n_union)
+            e = cudaMemcpy(st.d_union_ids, uni.data(), (size_t)st.n_union * 4,
+                           cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
             free_layers(ctx);
             return cuda_fail(ctx, e, "device ELT store");
@@ -663,7 +710,7 @@ ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_tr
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
-        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE))
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE | ARA_RUN_HOIST))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
         if (!out) return fail(ctx, ARA_ERR_ARG, "outputs is NULL");
         if (n_trials == 0) return ARA_OK;
@@ -698,6 +745,10 @@ ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_tr
             if (s != ARA_OK) return s;
         }
         const bool extra = o.max_occ || o.event_inc;
+        if ((flags & ARA_RUN_HOIST) && !extra) {
+            ara_status h = prepare_hoist(ctx);
+            if (h != ARA_OK) return h;
+        }
         ara_status s = launch_layers(ctx, n_trials, d_trial_offsets, d_event_ids, o.ylt, o.ylt_ld,
                                      flags, extra ? &o : nullptr);
         if (s != ARA_OK) return s;
@@ -727,7 +778,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
 {
     return guarded(ctx, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
-        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE))
+        if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE | ARA_RUN_HOIST))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
         if (n_trials == 0) return ARA_OK;
         if (!h_trial_offsets || !h_ylt) return fail(ctx, ARA_ERR_ARG, "host pointer is NULL");
@@ -751,6 +802,10 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
             ctx->ylt_stage_cap = 0;
             ARA_CUDA(ctx, cudaMalloc(&ctx->d_ylt_stage, n_layers * n_trials * 8));
             ctx->ylt_stage_cap = n_layers * n_trials;
+        }
+        if (flags & ARA_RUN_HOIST) {  // the per-event table once for all chunks
+            s = prepare_hoist(ctx);
+            if (s != ARA_OK) return s;
         }
         // chunking at trial boundaries: ~64 MiB of ids per chunk (>= 1 trial)
         const size_t kChunkIds = (size_t)16 << 20;

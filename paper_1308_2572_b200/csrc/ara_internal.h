@@ -122,6 +122,13 @@ struct DeviceStore {
     uint32_t zero_base_direct = 0;  // C + 1 (d_rows_direct)
     void *d_terms = nullptr;     // [n_layers] LayerTermsT<double or float>
     UnionStore uni;              // F1 union rows (when eligible)
+    // hoisted scan (hoist.cu, ARA_RUN_HOIST): per-event layer losses oc[row][l], allocated on
+    // the first hoisted run; rows are catalogue ids (oc_direct, map modes 1-2) or dense rows
+    uint32_t *d_union_ids = nullptr;  // [U]: dense row u+1 -> catalogue id
+    void *d_oc = nullptr;             // [(C+1) or (U+1)] x oc_lp, R; absent rows stay +0
+    int oc_direct = 0;
+    uint32_t oc_lp = 0;               // layers padded to 1, 2, 4 or 8
+    uint32_t *d_oc_bitmap = nullptr;  // map mode 2: 2^kBitmapLog2Hoist-bit presence bitmap
 };
 
 // Every row store ends with a block of kZeroRows all-zero rows (at DeviceStore / UnionStore
@@ -136,6 +143,7 @@ constexpr uint32_t kZeroRows = 1024;
 // b = 18 for the union-row kernel (its blocks also hold their F rows in shared memory).
 constexpr int kBitmapLog2Scan = 19;
 constexpr int kBitmapLog2Union = 18;
+constexpr int kBitmapLog2Hoist = 18;  // hoisted scan (hoist.cu): 32 KB, 2 blocks of 512 per SM
 __host__ __device__ inline uint32_t bitmap_hash(uint32_t id, uint32_t log2_bits)
 {
     return (id * 0x9E3779B1u) >> (32 - log2_bits);
@@ -179,6 +187,10 @@ cudaError_t launch_build_bitmap(const uint32_t *d_map, uint32_t C, uint32_t *bit
                                 uint32_t log2_bits, cudaStream_t stream);
 cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream, uint64_t *launches);
+// hoist.cu
+cudaError_t launch_hoist_oc(const DeviceStore &st, cudaStream_t stream, uint64_t *launches);
+cudaError_t launch_hoisted_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                                cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int map_mode,
                              const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
                              cudaStream_t stream, uint64_t *launches);

@@ -267,6 +267,73 @@ def test_portfolio_layer_sum_variants(stream, monkeypatch, kind, shfl_env):
     ctx.close()
 
 
+# --------------------------------------------------------------------------- hoisted scan
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("preset,kw", [
+    ("tiny", dict(n_trials=900, k_min=0, k_max=40)),                    # h = 0.5, empty trials
+    ("sweep-h10", dict(n_trials=1200, k_min=990, k_max=1010)),          # 90% absent ids
+    ("portfolio", dict(n_trials=400, k_min=100, k_max=300)),            # 8 layers (LP = 8)
+    ("portfolio", dict(n_trials=300, k_min=1, k_max=200, n_layers=3, elts_per_layer=12,
+                       layer_stride=5)),                                # LP = 4, padding layer
+    ("portfolio", dict(n_trials=300, k_min=9, k_max=17, n_layers=2)),   # LP = 2, short trials
+    ("sweep-e64", dict(n_trials=500, k_min=200, k_max=260)),
+    ("sweep-e4", dict(n_trials=500, k_min=7, k_max=700)),
+])
+def test_hoisted_scan(stream, monkeypatch, mode, preset, kw):
+    """ARA_RUN_HOIST (Alg. 1 lines 4-17 once per distinct event, then one table read per
+    occurrence and layer) gives the oracle's YLT bit for bit in every row-addressing mode, for
+    1-8 layers, ragged and empty trials and mostly-absent ids, on repeated runs (the table is
+    recomputed each run; absent entries stay zero) and through the host-buffer call."""
+    monkeypatch.setenv("ARA_MAP_MODE", str(mode))
+    ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
+    want = oracle.run_analysis(ds, n_threads=8)
+    ctx = make_ctx(ds, stream)
+    for flags in (ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST,
+                  ara.ARA_RUN_SYNC | ara.ARA_RUN_VALIDATE | ara.ARA_RUN_HOIST):
+        assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=flags), want)
+    h = np.full((ds.n_layers, ds.n_trials), np.nan)
+    ctx.ara_run_host(ds.trial_offsets, ds.events, h, flags=ara.ARA_RUN_HOIST)
+    assert_bit_identical(h, want)
+    ctx.close()
+
+
+@pytest.mark.parametrize("preset", ["tiny", "medium"])
+def test_hoisted_scan_f32(stream, preset):
+    """The hoisted scan in the fp32 variant (F3) equals the float oracle bit for bit."""
+    spec = datagen.PRESETS[preset].replace(n_trials=2000, k_min=0, k_max=300, seed=9)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds, n_threads=8, precision=32)
+    ctx = ara.Context(0, stream)
+    ctx.ara_set_precision(32)
+    ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx,
+                                 flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST), want)
+    ctx.close()
+
+
+def test_hoisted_scan_limits(stream):
+    """More than 8 layers: ARA_RUN_HOIST is refused with ARA_ERR_UNSUPPORTED (the full scan
+    still runs); an out-of-range id is reported as with the full scan."""
+    spec = datagen.PRESETS["portfolio"].replace(n_trials=50, k_min=5, k_max=9, n_layers=9,
+                                                elts_per_layer=4)
+    ds = datagen.generate(spec)
+    ctx = make_ctx(ds, stream)
+    with pytest.raises(ara.AraError) as ei:
+        gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST)
+    assert ei.value.status_name == "ARA_ERR_UNSUPPORTED"
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx), oracle.run_analysis(ds))
+    ctx.close()
+    ds = datagen.generate(datagen.PRESETS["tiny"].replace(n_trials=40))
+    ev = ds.events.copy()
+    ev[7] = ds.catalogue_size + 1
+    ctx = make_ctx(ds, stream)
+    with pytest.raises(ara.AraError) as ei:
+        gpu_ylt(ds, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST, events=ev)
+    assert ei.value.status_name == "ARA_ERR_RANGE"
+    ctx.close()
+
+
 # --------------------------------------------------------------------------- store (A1)
 @pytest.mark.parametrize("preset", ["tiny", "medium"])
 def test_store_round_trip(stream, preset):
@@ -561,9 +628,11 @@ def _sampled_oracle(spec, ds, sel):
     return oracle.run_analysis(ds, n_threads=8, trial_offsets=to, events=ev)
 
 
-@pytest.mark.parametrize("preset", ["portfolio", "sweep-e4", "sweep-e64", "sweep-k2000",
-                                    "sweep-ragged", "sweep-h10", "sweep-n8m"])
-def test_full_size_config_sampled(stream, preset):
+@pytest.mark.parametrize("preset,hoist", [
+    ("portfolio", False), ("sweep-e4", False), ("sweep-e64", False), ("sweep-k2000", False),
+    ("sweep-ragged", False), ("sweep-h10", False), ("sweep-n8m", False),
+    ("headline", True), ("portfolio", True), ("sweep-h10", True)])
+def test_full_size_config_sampled(stream, preset, hoist):
     """BASELINE.json configs[3] (8-layer portfolio, 1M x 1000) and the configs[4] sweep extremes
     (E = 4 and 64, k = 2000, k in 800-1500, 10% hit rate, 8M trials = 32 GB of ids) at full
     size, in the launch configuration bench.py times (default flags): the YET is generated
@@ -582,7 +651,8 @@ def test_full_size_config_sampled(stream, preset):
         d_ids[a:a + e.shape[0]].copy_(torch.from_numpy(e.view(np.int32)))
     ctx = make_ctx(ds, stream)
     ylt = torch.full((ds.n_layers, n), float("nan"), dtype=torch.float64, device=DEV)
-    ctx.ara_run(to_dev(off, "u64"), d_ids.view(torch.uint32), ylt)
+    ctx.ara_run(to_dev(off, "u64"), d_ids.view(torch.uint32), ylt,
+                flags=ara.ARA_RUN_HOIST if hoist else 0)
     ctx.ara_synchronize()
     got = ylt.cpu().numpy()
     ctx.close()
