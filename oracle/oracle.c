@@ -14,9 +14,12 @@
  *
  * Readings of the paper where it is silent / garbled (DESIGN.md "Readings" R1-R12):
  *   R1 ApplyFinancialTerms(I) = min(max(x*rate - retention, 0), limit)   (
- *      SPEC.md L216-L224).  PARITY UNPINNED against the paper itself: the paper never
- *      defines I beyond "currency exchange rates and terms"; pinned only by SPEC's
- *      hand-derived examples and by the XL-layer interval characterisation in tests.
+ *      SPEC.md L216-L224).  The paper never defines I beyond "currency exchange rates and
+ *      terms", so WHICH terms I holds is a reading (SPEC's); the oracle's implementation of
+ *      that reading is pinned by tests independent of this file: SPEC's hand-derived
+ *      examples, the exhaustive excess-of-loss interval characterisation |[0,x] n [R,R+L]|
+ *      in exact rationals, the stop-loss / per-occurrence-XL special cases and the
+ *      separate-rounding (no FMA) check.
  *   R2 line 6: x_d = loss of occurrence d's event in ELT c, 0 if absent.
  *   R3 lo/l are indexed by occurrence position d (repeated events charged per occurrence).
  *   R4 lo = 0 and lr = 0 per (layer, trial); YLT[a][t] = lr after line 29.

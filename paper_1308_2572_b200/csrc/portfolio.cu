@@ -134,6 +134,18 @@ __global__ void __launch_bounds__(kScanThreads, 3)
 #pragma unroll
             for (int i = 0; i < kUnionMaxE; ++i) {
                 const uint32_t sl = src5[i / 6] >> (5 * (i % 6));
+#if defined(ARA_PF_PTX_ADD)
+                if constexpr (SH == 2) {
+                    asm("{\n\t.reg .b32 l32, h32;\n\t.reg .f64 v;\n\t"
+                        "mov.b64 {l32, h32}, %2;\n\t"
+                        "shfl.sync.idx.b32 l32, l32, %3, %4, %5;\n\t"
+                        "shfl.sync.idx.b32 h32, h32, %3, %4, %5;\n\t"
+                        "mov.b64 v, {l32, h32};\n\tadd.rn.f64 %0, %1, v;\n\t}"
+                        : "=d"(lo) : "d"(lo), "d"(f[i % 8]), "r"(sl),
+                          "n"(((32 - GU) << 8) | 0x1f), "r"(gmask));
+                    continue;
+                }
+#endif
                 double v = __shfl_sync(gmask, f[i % 8], sl, GU);
                 if (SH == 1) v = (uint32_t)i < my_n ? v : 0.0;  // past the layer's ELTs: +0
                 lo = radd(lo, v);
