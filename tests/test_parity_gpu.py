@@ -631,7 +631,8 @@ def _sampled_oracle(spec, ds, sel):
 @pytest.mark.parametrize("preset,hoist", [
     ("portfolio", False), ("sweep-e4", False), ("sweep-e64", False), ("sweep-k2000", False),
     ("sweep-ragged", False), ("sweep-h10", False), ("sweep-n8m", False),
-    ("headline", True), ("portfolio", True), ("sweep-h10", True)])
+    ("sweep-bigstore", False),
+    ("headline", True), ("portfolio", True), ("sweep-h10", True), ("sweep-bigstore", True)])
 def test_full_size_config_sampled(stream, preset, hoist):
     """BASELINE.json configs[3] (8-layer portfolio, 1M x 1000) and the configs[4] sweep extremes
     (E = 4 and 64, k = 2000, k in 800-1500, 10% hit rate, 8M trials = 32 GB of ids) at full
