@@ -40,7 +40,13 @@ struct ara_ctx {
 
     uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
     unsigned long long *d_ticket = nullptr;  // dynamic scheduling: ticket + done counters
+    unsigned long long *d_probe = nullptr;  // map mode 2: hit-probe counts of the current run
+    unsigned long long *h_probe = nullptr;  // pinned copy of the last probe (read one run later)
+    cudaEvent_t ev_probe = nullptr;
+    bool probe_pending = false;             // a copy into h_probe is in flight
+    bool probe_mode1 = false;               // the last completed probe said ">= 99% present"
     int sched = 0;              // 0 auto, 1 static, 2 dynamic (env ARA_SCAN_SCHED)
+    bool probe = true;          // map mode 2 hit probe (env ARA_MAP_PROBE=0 disables)
     int bits = 64;              // store / arithmetic precision (ara_set_precision)
     uint32_t *h_err = nullptr;  // pinned mirror
     uint64_t launches = 0;
@@ -119,6 +125,7 @@ void free_layers(ara_ctx *ctx)
     cudaFree(ctx->store.d_oc_bitmap);
     ctx->store = ara::DeviceStore();
     ctx->store_bytes = 0;
+    ctx->probe_mode1 = false;  // a new store: no probe verdict yet
     ctx->have_layers = false;
 }
 
@@ -225,16 +232,63 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                       dyn ? ctx->d_ticket : nullptr,
                       dyn ? (unsigned int *)(ctx->d_ticket + 1) : nullptr,
                       extra ? extra->max_occ : nullptr, extra ? extra->max_occ_ld : 0,
-                      extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm};
+                      extra ? extra->event_inc : nullptr, extra ? extra->event_inc_ld : 0, perm,
+                      nullptr};
+    // Map mode 2 (direct rows behind the presence bitmap): a probe of the YET's hit rate lets
+    // the scan skip the bitmap test when (nearly) every id is in the store; results do not
+    // depend on it.  ARA_MAP_PROBE=0 disables the probe (tuning).
+    // The kernels read the probe on the device and run their mode-1 body when >= 99% of the
+    // sampled ids are present.  The host also reads the PREVIOUS run's probe counts (copied back
+    // asynchronously, never waited for): when they said "present" it launches the plain mode-1
+    // kernel, which is ~3% faster than the combined one (a perf heuristic only: every mode gives
+    // the same YLT, so a stale verdict is never wrong).
     const bool hoist = (flags & ARA_RUN_HOIST) && !extra;
-    cudaError_t e =
-        hoist ? ara::launch_hoisted_scan(ctx->store, s, ctx->sm_count, ctx->stream,
-                                         &ctx->launches)
-        : (ctx->store.uni.enabled && !extra)
-            ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, ctx->store.map_mode,
-                                    ctx->store.d_bitmap, s, ctx->sm_count, ctx->stream,
-                                    &ctx->launches)
-            : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
+    const bool hoist_bm = hoist && ctx->store.d_oc_bitmap;
+    bool mode1 = false;
+    if (!extra && ctx->probe && (ctx->store.map_mode == 2 || hoist_bm)) {
+        if (ctx->probe_pending) {
+            const cudaError_t q = cudaEventQuery(ctx->ev_probe);
+            if (q == cudaSuccess) {
+                const unsigned long long hit = ctx->h_probe[0], cnt = ctx->h_probe[1];
+                ctx->probe_mode1 = cnt > 0 && 100ull * hit >= 99ull * cnt;
+                ctx->probe_pending = false;
+            } else if (q == cudaErrorNotReady) {
+                cudaGetLastError();  // "not ready" is not an error; keep it out of the launch checks
+            } else {
+                return cuda_fail(ctx, q, "hit probe event");
+            }
+        }
+        mode1 = ctx->probe_mode1;
+        cudaError_t pe = ara::launch_hit_probe(d_off, d_ids, n, ctx->store.d_map, ctx->C,
+                                               ctx->d_probe, ctx->stream, &ctx->launches);
+        if (pe == cudaSuccess && !ctx->probe_pending) {
+            pe = cudaMemcpyAsync(ctx->h_probe, ctx->d_probe, 16, cudaMemcpyDeviceToHost,
+                                 ctx->stream);
+            if (pe == cudaSuccess) pe = cudaEventRecord(ctx->ev_probe, ctx->stream);
+            ctx->probe_pending = pe == cudaSuccess;
+        }
+        if (pe != cudaSuccess) return cuda_fail(ctx, pe, "hit probe");
+        s.probe = ctx->d_probe;
+    }
+    cudaError_t e;
+    if (mode1) {  // a store view addressed like map mode 1 (same buffers)
+        ara::DeviceStore st1 = ctx->store;
+        st1.map_mode = 1;
+        st1.d_oc_bitmap = nullptr;
+        e = hoist ? ara::launch_hoisted_scan(st1, s, ctx->sm_count, ctx->stream, &ctx->launches)
+            : st1.uni.enabled
+                ? ara::launch_portfolio(st1.uni, st1.d_map, 1, st1.d_bitmap, s, ctx->sm_count,
+                                        ctx->stream, &ctx->launches)
+                : ara::launch_scan(st1, s, ctx->sm_count, ctx->stream, &ctx->launches);
+    } else {
+        e = hoist ? ara::launch_hoisted_scan(ctx->store, s, ctx->sm_count, ctx->stream,
+                                             &ctx->launches)
+            : (ctx->store.uni.enabled && !extra)
+                ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, ctx->store.map_mode,
+                                        ctx->store.d_bitmap, s, ctx->sm_count, ctx->stream,
+                                        &ctx->launches)
+                : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
 }
@@ -475,8 +529,13 @@ ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
     if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_ticket, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_ticket, 0, 16);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_probe, 16);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_probe, 0, 16);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_probe, 16);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_probe, cudaEventDisableTiming);
     if (const char *sc = getenv("ARA_SCAN_SCHED"))
         ctx->sched = strcmp(sc, "static") == 0 ? 1 : strcmp(sc, "dynamic") == 0 ? 2 : 0;
+    if (const char *pr = getenv("ARA_MAP_PROBE")) ctx->probe = atoi(pr) != 0;
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, 4);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
     for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
@@ -522,6 +581,9 @@ void ara_destroy(ara_ctx *ctx)
     free_layers(ctx);
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_ticket);
+    cudaFree(ctx->d_probe);
+    cudaFreeHost(ctx->h_probe);
+    if (ctx->ev_probe) cudaEventDestroy(ctx->ev_probe);
     cudaFreeHost(ctx->h_err);
     cudaFree(ctx->metrics.d_buf);
     cudaFree(ctx->sort.d_buf);

@@ -167,6 +167,7 @@ struct ScanLaunch {
     double *event_inc;            // F4: [n_layers][event_inc_ld] or NULL (YET positions)
     uint64_t event_inc_ld;
     const uint32_t *perm;         // length-sorted trial order (ARA_RUN_BALANCE) or NULL
+    const unsigned long long *probe;  // map mode 2: hit-probe counts {present, sampled} or NULL
 };
 
 // Scratch of the length sort (ARA_RUN_BALANCE): keys, indices, CUB temporary storage.
@@ -193,6 +194,13 @@ cudaError_t launch_hoisted_scan(const DeviceStore &st, const ScanLaunch &s, int 
                                 cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int map_mode,
                              const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
+                             cudaStream_t stream, uint64_t *launches);
+// Map mode 2: sample up to kProbeSamples of the YET's event ids (evenly strided) and count how
+// many are in the store (probe[0]) of how many sampled (probe[1]); the scans skip their
+// presence-bitmap test when at least 99% are (probe_use_bitmap).
+constexpr uint32_t kProbeSamples = 65536;
+cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
+                             const uint32_t *d_map, uint32_t C, unsigned long long *probe,
                              cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
                             uint32_t catalogue_size, uint32_t *err, int sm_count,

@@ -111,10 +111,12 @@ __device__ __forceinline__ bool oc_row(const RowLookup &L, uint32_t id, bool &ba
 }
 
 template <int LP, typename R, bool BAL, int MM>
-__global__ void __launch_bounds__(hoist_threads<LP>())
-    hoisted_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                        const uint32_t *__restrict__ bitmap, const R *__restrict__ oc,
-                        const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
+__device__ __forceinline__ void hoisted_body(const ScanLaunch &s,
+                                             const uint32_t *__restrict__ map,
+                                             const uint32_t *__restrict__ bitmap,
+                                             const R *__restrict__ oc,
+                                             const LayerTermsT<R> *__restrict__ terms,
+                                             uint32_t n_layers)
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
@@ -222,6 +224,22 @@ __global__ void __launch_bounds__(hoist_threads<LP>())
             }
         }
     }
+}
+
+// Map mode 2 runs the mode-1 body when the hit probe found (nearly) every sampled id present.
+template <int LP, typename R, bool BAL, int MM>
+__global__ void __launch_bounds__(hoist_threads<LP>())
+    hoisted_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
+                        const uint32_t *__restrict__ bitmap, const R *__restrict__ oc,
+                        const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
+{
+    if constexpr (MM == 2) {
+        if (!probe_use_bitmap(s.probe)) {
+            hoisted_body<LP, R, BAL, 1>(s, map, bitmap, oc, terms, n_layers);
+            return;
+        }
+    }
+    hoisted_body<LP, R, BAL, MM>(s, map, bitmap, oc, terms, n_layers);
 }
 
 template <int LP, typename R, bool BAL, int MM>

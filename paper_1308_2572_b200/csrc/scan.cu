@@ -41,7 +41,7 @@ __device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
                                            const R (&ret)[Chunk<R>::N * CH],
                                            const R (&lim)[Chunk<R>::N * CH], uint32_t gmask,
                                            R occ_ret, R occ_lim, R agg_ret, R agg_lim, R &S,
-                                           R &Cprev, R &lr, R &oc_out, R &inc_out)
+                                           R &Cprev, R &lr, R &oc_out, R &inc_out, R &own)
 {
     constexpr int PER = Chunk<R>::N;
     constexpr int NCOL = PER * CH;
@@ -59,6 +59,7 @@ __device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
     R part = R(0);
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) part = radd(part, f[j]);
+    own = part;  // this lane's columns only: available before the chain through the group
 #pragma unroll
     for (int h = 1; h < G; ++h) {
         R x = __shfl_up_sync(gmask, part, 1, G);  // lane h reads lane h-1
@@ -98,11 +99,12 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
     for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
 }
 
-template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D = 2>
-__global__ void __launch_bounds__(kScanThreads, MINB)
-    scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
-                const uint32_t *__restrict__ bitmap, const R *__restrict__ rows,
-                const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
+template <int G, int CH, bool X, typename R, bool BAL, int MM, int D>
+__device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
+                                          const uint32_t *__restrict__ bitmap,
+                                          const R *__restrict__ rows,
+                                          const LayerTermsT<R> *__restrict__ terms,
+                                          uint32_t n_layers)
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
         const uint32_t *const ev_end = ev + k;
         R S = 0, Cprev = 0, lr = 0;  // lines 19, 25 (C_0 = 0), 28
         R max_oc = 0, oc, inc;       // F4
+        R own = 0;                   // last event's own-column partial (gather pin)
         const bool writer = c == G - 1;
 
         // head: single events until the id pointer is 32-byte aligned
@@ -182,7 +185,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             Chunk<R> r[CH];
             gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
-                              Cprev, lr, oc, inc);
+                              Cprev, lr, oc, inc, own);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
@@ -209,13 +212,13 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         event_step<G, CH, R>(ring[j % D], rate, ret, lim, gmask, occ_ret, occ_lim,
-                                             agg_ret, agg_lim, S, Cprev, lr, oc, inc);
+                                             agg_ret, agg_lim, S, Cprev, lr, oc, inc, own);
                         event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                         const int e2 = j + D;  // refill: event j + D of this chunk or the next
                         const uint32_t id2 = e2 < 8 ? id_c[e2 < 8 ? e2 : 0] : id_n[e2 < 8 ? 0 : e2 - 8];
                         const bool ok2 = e2 < 8 || more;
                         const uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
-                        gather<CH, R>(my_rows, row_stride, pin(idx2, S), ring[j % D]);
+                        gather<CH, R>(my_rows, row_stride, pin(idx2, own), ring[j % D]);
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
@@ -242,14 +245,14 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
                     const bool ok2 = j + 2 < 8 || more;
                     uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
                     Chunk<R> rb[CH];
-                    gather<CH, R>(my_rows, row_stride, pin(idx1, S), rb);
+                    gather<CH, R>(my_rows, row_stride, pin(idx1, own), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
-                                      agg_lim, S, Cprev, lr, oc, inc);
+                                      agg_lim, S, Cprev, lr, oc, inc, own);
                     event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                     uint32_t idx3 = ok2 ? row_index<MM>(look, id3, bad) : zb;
-                    gather<CH, R>(my_rows, row_stride, pin(idx2, S), ra);  // event j+2 (zero row past end)
+                    gather<CH, R>(my_rows, row_stride, pin(idx2, own), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
-                                      agg_lim, S, Cprev, lr, oc, inc);
+                                      agg_lim, S, Cprev, lr, oc, inc, own);
                     event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1, writer);
                     idx1 = idx3;
                 }
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
             Chunk<R> r[CH];
             gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
-                              Cprev, lr, oc, inc);
+                              Cprev, lr, oc, inc, own);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
             ++ev;
         }
@@ -300,6 +303,23 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     }
 }
 
+// The kernel: map mode 2 runs its mode-1 body when the hit probe found (nearly) every sampled
+// id in the store (probe_use_bitmap), chosen once per launch.
+template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D = 2>
+__global__ void __launch_bounds__(kScanThreads, MINB)
+    scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
+                const uint32_t *__restrict__ bitmap, const R *__restrict__ rows,
+                const LayerTermsT<R> *__restrict__ terms, uint32_t n_layers)
+{
+    if constexpr (MM == 2) {
+        if (!probe_use_bitmap(s.probe)) {
+            scan_body<G, CH, X, R, BAL, 1, D>(s, map, bitmap, rows, terms, n_layers);
+            return;
+        }
+    }
+    scan_body<G, CH, X, R, BAL, MM, D>(s, map, bitmap, rows, terms, n_layers);
+}
+
 // Device-side validation (ARA_RUN_VALIDATE): offsets non-decreasing, ids in [1, C].
 __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
                                 const uint32_t *__restrict__ ids, uint64_t n_trials,
@@ -318,6 +338,31 @@ __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
     for (uint64_t i = tid; i < n_ev; i += stride)
         if (ids[i] - 1u >= C) e |= kErrRange;
     if (e) atomicOr(err, e);
+}
+
+// Map-mode-2 hit probe (launch_hit_probe): one thread per sampled id, evenly strided over the
+// YET (the samples are independent DRAM reads: one per thread keeps them all in flight).
+// probe[0] = sampled ids present in the store, probe[1] = ids sampled (zeroed before launch).
+__global__ void __launch_bounds__(256) hit_probe_kernel(const uint64_t *__restrict__ offsets,
+                                                        const uint32_t *__restrict__ ids,
+                                                        uint64_t n_trials,
+                                                        const uint32_t *__restrict__ map,
+                                                        uint32_t C, unsigned long long *probe)
+{
+    const uint64_t n_ev = offsets[n_trials] - offsets[0];
+    const uint64_t m = n_ev < kProbeSamples ? n_ev : kProbeSamples;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool hit = false;
+    if (i < m) {
+        const uint32_t id = ids[i * (n_ev / m)];
+        hit = (id - 1u) < C && map[id] != 0u;
+    }
+    const uint32_t nh = __popc(__ballot_sync(0xffffffffu, hit));
+    const uint32_t nc = __popc(__ballot_sync(0xffffffffu, i < m));
+    if ((threadIdx.x & 31u) == 0 && nc) {
+        atomicAdd(probe, (unsigned long long)nh);
+        atomicAdd(probe + 1, (unsigned long long)nc);
+    }
 }
 
 // Keys for the length sort: trial lengths (saturated to 32 bits) and trial indices.
@@ -450,7 +495,7 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
         }
         switch (st.width) {
             case 4: return launch_gc<1, 1, 1, false, double, true>(st, s, sm_count, stream);
-            case 8: return launch_gc<2, 1, 1, false, double, true>(st, s, sm_count, stream);
+            case 8: return launch_gc<2, 1, 4, false, double, true>(st, s, sm_count, stream);
             case 16:  // tuning variants: ARA_SCAN_GROUP (G), ARA_SCAN_DEPTH (D), ARA_SCAN_MINB
                 if (st.group_override == 4) {
                     if (st.depth == 8)
@@ -467,7 +512,7 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
             case 32:
                 if (st.group_override == 8)
                     return launch_gc<8, 1, 4, false, double, true>(st, s, sm_count, stream);
-                return launch_gc<4, 2, 1, false, double, true>(st, s, sm_count, stream);
+                return launch_gc<4, 2, 3, false, double, true>(st, s, sm_count, stream);
             case 48: return launch_gc<4, 3, 1, false, double, true>(st, s, sm_count, stream);
             case 64:
                 if (st.group_override == 8)
@@ -555,6 +600,19 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
                                                   (int)n, 0, 32, stream);
     sc.perm = idx_out;
     return e;
+}
+
+cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
+                             const uint32_t *d_map, uint32_t C, unsigned long long *probe,
+                             cudaStream_t stream, uint64_t *launches)
+{
+    if (n_trials == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(probe, 0, 16, stream);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    hit_probe_kernel<<<kProbeSamples / 256, 256, 0, stream>>>(offsets, ids, n_trials, d_map, C,
+                                                               probe);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,

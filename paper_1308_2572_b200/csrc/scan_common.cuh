@@ -101,6 +101,17 @@ struct RowLookup {
     uint32_t bitmap_log2;              // mode 2: log2 of the bitmap's bit count
 };
 
+// Mode 2, per launch: consult the bitmap unless the hit probe (ScanLaunch::probe, written by
+// hit_probe_kernel before the scan) says >= 99% of the YET's sampled ids are in the store; the
+// kernels then run their mode-1 body (a separate instantiation chosen once at kernel entry --
+// a per-event runtime test in the hot loop cost 20%).
+__device__ __forceinline__ bool probe_use_bitmap(const unsigned long long *probe)
+{
+    if (probe == nullptr) return true;
+    const unsigned long long hit = probe[0], cnt = probe[1];
+    return !(cnt > 0 && 100ull * hit >= 99ull * cnt);
+}
+
 template <int MM>
 __device__ __forceinline__ uint32_t row_index(const RowLookup &L, uint32_t id, bool &bad)
 {
@@ -134,7 +145,10 @@ __device__ __forceinline__ void load_bitmap(uint32_t *sbits, const uint32_t *__r
 // gives the row index a true data dependency on such a value v (min with 2^32 - 1 - signbit(v),
 // which leaves every row index unchanged because indices are < 2^32 - 1); without it ptxas
 // hoists the gathers of an unrolled chunk above the arithmetic that frees their registers and
-// runs out of registers.
+// runs out of registers.  v must be the EARLIEST value computed from the slot's data (the
+// lane's own-column partial sum, or an F value), not the end of the event's serial chain (the
+// running sum S): pinning on S serialised every event's gather behind the previous event's
+// shuffle + occurrence/aggregate chain.
 __device__ __forceinline__ uint32_t pin(uint32_t idx, double v)
 {
     const uint32_t sbit = (uint32_t)__double2hiint(v) >> 31;

@@ -203,11 +203,15 @@ def test_absent_events_only(stream):
     ("tiny", dict(n_trials=500, k_min=50, k_max=300, catalogue_size=(1 << 21) + 777,
                   pool_size=30_000, records_per_elt=20_000)),  # ~6% of absent ids alias a set bit
 ])
-def test_row_addressing_modes(stream, monkeypatch, mode, preset, kw):
+@pytest.mark.parametrize("probe", ["1", "0"])
+def test_row_addressing_modes(stream, monkeypatch, mode, preset, kw, probe):
     """Every row-addressing mode (catalogue map, rows by catalogue id, id rows behind the
     shared-memory presence bitmap) gives the oracle's YLT bit for bit, including catalogues larger
     than the bitmap (hash collisions read the direct store's zero rows) and out-of-pool ids."""
     monkeypatch.setenv("ARA_MAP_MODE", str(mode))
+    monkeypatch.setenv("ARA_MAP_PROBE", probe)  # mode 2: hit probe on (may skip the bitmap)/off
+    if mode != 2 and probe == "0":
+        pytest.skip("the probe only matters in map mode 2")
     ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
     if ds.catalogue_size > (1 << 21):  # the case is meant to exercise bitmap collisions
         h = lambda ids: (ids.astype(np.uint64) * 0x9E3779B1 % (1 << 32)) >> 13  # noqa: E731
@@ -265,6 +269,21 @@ def test_portfolio_layer_sum_variants(stream, monkeypatch, kind, shfl_env):
     assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx), want)
     assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
     ctx.close()
+
+
+def test_hit_probe_threshold(stream, monkeypatch):
+    """Map mode 2 with a YET whose sampled hit rate is just above the probe's 99% threshold: the
+    scan skips the bitmap, so the ~0.5% absent ids read zero rows of the direct store -- the YLT
+    is still the oracle's bit for bit (full scan, union-row kernel and hoisted scan)."""
+    monkeypatch.setenv("ARA_MAP_MODE", "2")
+    for preset in ("medium", "portfolio"):
+        ds = datagen.generate(datagen.PRESETS[preset].replace(n_trials=3000, k_min=50, k_max=400,
+                                                              hit=0.995, seed=77))
+        want = oracle.run_analysis(ds, n_threads=8)
+        ctx = make_ctx(ds, stream)
+        for flags in (ara.ARA_RUN_SYNC, ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST):
+            assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=flags), want)
+        ctx.close()
 
 
 # --------------------------------------------------------------------------- hoisted scan
@@ -457,8 +476,9 @@ def test_errors(stream):
         ctx.ara_metrics(ylt[0], [1.0])
     n0 = ctx.kernel_launches
     ctx.ara_run(off, ev, ylt, flags=ara.ARA_RUN_SYNC)
-    # one scan launch covers every layer; the default schedule adds the length keys + sort
-    assert ctx.kernel_launches == n0 + 3
+    # one scan launch covers every layer; the default schedule adds the length keys + sort,
+    # map mode 2 the hit probe
+    assert ctx.kernel_launches == n0 + 3 + (ctx.ara_get_info().row_addressing == 2)
     ctx.close()
 
 
