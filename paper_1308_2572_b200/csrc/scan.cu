@@ -486,10 +486,12 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
     if (s.perm && !(s.max_occ || s.event_inc)) {  // length-bucketed (ARA_RUN_BALANCE)
         if (st.bits == 32) {
             switch (st.width) {
-                case 8: return launch_gc<1, 1, 1, false, float, true>(st, s, sm_count, stream);
-                case 16: return launch_gc<2, 1, 1, false, float, true>(st, s, sm_count, stream);
-                case 32: return launch_gc<2, 2, 1, false, float, true>(st, s, sm_count, stream);
-                case 64: return launch_gc<4, 2, 1, false, float, true>(st, s, sm_count, stream);
+                // register caps (__launch_bounds__ min blocks): without them ptxas spends up to
+                // 254 registers on deeper pipelining and halves the resident warps
+                case 8: return launch_gc<1, 1, 4, false, float, true>(st, s, sm_count, stream);
+                case 16: return launch_gc<2, 1, 4, false, float, true>(st, s, sm_count, stream);
+                case 32: return launch_gc<2, 2, 2, false, float, true>(st, s, sm_count, stream);
+                case 64: return launch_gc<4, 2, 2, false, float, true>(st, s, sm_count, stream);
                 default: --*launches; return cudaErrorInvalidValue;
             }
         }
