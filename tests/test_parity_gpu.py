@@ -686,3 +686,76 @@ def test_full_size_config_sampled(stream, preset, hoist):
     sel = np.concatenate([[0, n - 1], rng.choice(n, 1000, replace=False)]).astype(np.int64)
     want = _sampled_oracle(spec, ds, sel)
     assert_bit_identical(got[:, sel], want)
+
+
+# --------------------------------------------------------------------------- fuzz
+def _fuzz_dataset(seed: int, f32: bool):
+    """A random small portfolio: 1-10 layers of 1-64 ELTs in random order, random record sets
+    (including empty ELTs), loss scales from 1e-3 to 1e12 (1e-3 to 1e6 for fp32), terms drawn
+    from {0, +inf, exact dyadics, random}, ragged trials of 0-80 events (a few of ~1000), hit
+    rates 0-1, catalogues of 50-5000 ids (one case above the 2^21-bit presence bitmap)."""
+    rng = np.random.default_rng(seed)
+    pick = lambda choices: choices[int(rng.integers(0, len(choices)))]  # noqa: E731
+    C = int(rng.choice([50, 300, 5000, (1 << 21) + 13])) if seed % 9 else int(rng.integers(50, 400))
+    n_elts = int(rng.integers(1, 71))
+    top = 1e6 if f32 else 1e12
+    elts = []
+    for _ in range(n_elts):
+        m = int(rng.integers(0, min(C, 300) + 1))
+        ids = rng.choice(np.arange(1, C + 1), size=m, replace=False)
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            ls = np.exp(rng.uniform(np.log(1e-3), np.log(top), m))
+        elif kind == 1:
+            ls = rng.integers(1, 1 << 20, m).astype(float) / 64.0  # exact dyadics
+        else:
+            ls = rng.lognormal(8, 2, m)
+        rate = pick([1.0, 0.5, 1.25, float(rng.uniform(0.1, 3))])
+        ret = pick([0.0, float(np.median(ls)) if m else 0.0, float(rng.uniform(0, 1e4))])
+        lim = pick([math.inf, 0.0, float(rng.uniform(1, 1e5)), float(np.max(ls)) if m else 1.0])
+        elts.append({"records": list(zip(ids.tolist(), ls.tolist())), "fin": (rate, ret, lim)})
+    n_layers = int(rng.integers(1, 11))
+    layers = []
+    for _ in range(n_layers):
+        E = int(rng.integers(1, min(64, n_elts) + 1))
+        js = rng.choice(n_elts, size=E, replace=False).tolist()
+        scale = float(rng.choice([1e2, 1e4, 1e6]))
+        t = [pick([0.0, scale * float(rng.uniform(0, 2))]),
+             pick([math.inf, 0.0, scale * float(rng.uniform(0.1, 5))]),
+             pick([0.0, scale * float(rng.uniform(0, 50))]),
+             pick([math.inf, 0.0, scale * float(rng.uniform(1, 100))])]
+        layers.append({"elts": js, "terms": t})
+    n = int(rng.integers(1, 500))
+    hit = float(rng.uniform(0, 1))
+    present = np.unique(np.concatenate([np.array([i for i, _ in e["records"]], dtype=np.int64)
+                                        for e in elts] + [np.zeros(0, np.int64)]))
+    trials = []
+    for _ in range(n):
+        k = int(rng.integers(0, 81)) if rng.random() > 0.02 else int(rng.integers(900, 1100))
+        from_pool = rng.random(k) < hit
+        ev = rng.integers(1, C + 1, k)
+        if present.size:
+            ev[from_pool] = rng.choice(present, size=int(from_pool.sum()))
+        trials.append(ev.tolist())
+    return make_dataset(C, elts, layers, trials)
+
+
+@pytest.mark.parametrize("seed", range(36))
+def test_fuzz_parity(stream, monkeypatch, seed):
+    """Random portfolios (see _fuzz_dataset) through every path the configuration admits --
+    full scan in a random map mode with the default and the static schedule, the hoisted scan,
+    the fp32 variant every third case -- bit-identical to the oracle of the same precision."""
+    f32 = seed % 3 == 2
+    ds = _fuzz_dataset(1000 + seed, f32)
+    monkeypatch.setenv("ARA_MAP_MODE", str(seed % 3))
+    want = oracle.run_analysis(ds, n_threads=8, precision=32 if f32 else 64)
+    ctx = ara.Context(0, stream)
+    if f32:
+        ctx.ara_set_precision(32)
+    ctx.ara_load_elts(ds.catalogue_size, ds.rec_offsets, ds.rec_event_ids, ds.rec_losses, ds.fin)
+    ctx.ara_set_layers(ds.layer_terms, ds.elt_offsets, ds.elt_index)
+    assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx), want)
+    if ds.n_layers <= 8:
+        assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx,
+                                     flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST), want)
+    ctx.close()
