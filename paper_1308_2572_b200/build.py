@@ -57,8 +57,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
     if not variant and not force and not _stale():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    for src in _sources():
+    objs, procs = [], []
+    for src in _sources():  # the translation units compile in parallel
         name = os.path.basename(src)
         obj = os.path.join(BUILD, (f"{variant}_" if variant else "") + name + ".o")
         cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], *PER_FILE[name], "-c", src,
@@ -66,15 +66,21 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
         if src.endswith(".cpp"):
             cmd = [NVCC, *COMMON, *[f"-D{d}" for d in defines], "-x", "cu", *ARCH, "-c", src,
                    "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        with open(os.path.join(BUILD, f"ptxas_{variant}{name}.txt"), "w") as f:
-            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed for {name}")
-        if verbose:
-            sys.stdout.write(r.stderr)
+        procs.append((name, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                                  stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
+    failed = None
+    for name, cmd, pr in procs:
+        out, err = pr.communicate()
+        with open(os.path.join(BUILD, f"ptxas_{variant}{name}.txt"), "w") as f:
+            f.write(" ".join(cmd) + "\n" + out + err)
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            failed = failed or name
+        elif verbose:
+            sys.stdout.write(err)
+    if failed:
+        raise RuntimeError(f"nvcc failed for {failed}")
     tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
     os.replace(tmp, lib)
