@@ -40,11 +40,16 @@ struct ara_ctx {
 
     uint32_t *d_err = nullptr;  // device error word (ara::kErr*)
     unsigned long long *d_ticket = nullptr;  // dynamic scheduling: ticket + done counters
-    unsigned long long *d_probe = nullptr;  // map mode 2: hit-probe counts of the current run
-    unsigned long long *h_probe = nullptr;  // pinned copy of the last probe (read one run later)
+    // Per-run statistics on the device: [0] hit-probe ids present, [1] ids sampled (map mode
+    // 2), [2] trial lengths not all equal, [3] set when [2] was measured.  Copied back
+    // asynchronously and read by the host one run later (never waited for): performance
+    // heuristics only -- every choice they drive gives the same YLT.
+    unsigned long long *d_probe = nullptr;
+    unsigned long long *h_probe = nullptr;  // pinned copy of the last completed run's stats
     cudaEvent_t ev_probe = nullptr;
     bool probe_pending = false;             // a copy into h_probe is in flight
-    bool probe_mode1 = false;               // the last completed probe said ">= 99% present"
+    bool probe_mode1 = false;               // the last probe said ">= 99% present"
+    bool lengths_equal = false;             // the last check said "all trials equally long"
     int sched = 0;              // 0 auto, 1 static, 2 dynamic (env ARA_SCAN_SCHED)
     bool probe = true;          // map mode 2 hit probe (env ARA_MAP_PROBE=0 disables)
     int bits = 64;              // store / arithmetic precision (ara_set_precision)
@@ -218,13 +223,44 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     // nearly equal length (variable-length YETs keep full SIMT width; measured neutral for
     // equal lengths, profiles/README.md).  ARA_SCAN_SCHED=static|dynamic selects the plain
     // round-robin / per-group ticket schedules (tuning); the F4 outputs use per-group tickets.
+    const bool hoist = (flags & ARA_RUN_HOIST) && !extra;
+    const bool hoist_bm = hoist && ctx->store.d_oc_bitmap;
+    const bool probing = !extra && ctx->probe && (ctx->store.map_mode == 2 || hoist_bm);
+    // the previous run's statistics, if their copy has landed
+    if (ctx->probe_pending) {
+        const cudaError_t q = cudaEventQuery(ctx->ev_probe);
+        if (q == cudaSuccess) {
+            const unsigned long long *h = ctx->h_probe;
+            if (h[1] > 0) ctx->probe_mode1 = 100ull * h[0] >= 99ull * h[1];
+            if (h[3]) ctx->lengths_equal = h[2] == 0;
+            ctx->probe_pending = false;
+        } else if (q == cudaErrorNotReady) {
+            cudaGetLastError();  // "not ready" is not an error; keep it out of the launch checks
+        } else {
+            return cuda_fail(ctx, q, "run statistics event");
+        }
+    }
+    ARA_CUDA(ctx, cudaMemsetAsync(ctx->d_probe, 0, 32, ctx->stream));
+    // Scheduling (results are identical either way).  Default: trials sorted by length on the
+    // device and handed out in warp-sized batches, so the thread groups of a warp run trials of
+    // nearly equal length (variable-length YETs keep full SIMT width; measured neutral for
+    // equal lengths, profiles/README.md).  When the previous run's trials were all equally long
+    // the sort is skipped (identity order; a cheap check keeps the verdict current).
+    // ARA_SCAN_SCHED=static|dynamic selects the plain round-robin / per-group ticket schedules
+    // (tuning); the F4 outputs use per-group tickets.
     const bool balance = ctx->sched == 0 && !extra && n <= 0xffffffffull;  // u32 permutation
+    const bool sorted = balance && !ctx->lengths_equal;
     const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
     const uint32_t *perm = nullptr;
-    if (balance) {
+    if (sorted) {
         cudaError_t e = ara::launch_length_sort(d_off, n, ctx->sort, ctx->sm_count, ctx->stream,
-                                                &ctx->launches);
+                                                &ctx->launches, ctx->d_probe + 2);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "length sort");
+        perm = ctx->sort.perm;
+    } else if (balance) {  // equally long trials: identity order, same warp-batched kernel
+        cudaError_t e = ara::launch_length_check(d_off, n, ctx->sort, ctx->d_probe + 2,
+                                                 ctx->sm_count, ctx->stream, &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "length check");
         perm = ctx->sort.perm;
     }
     ara::ScanLaunch s{d_off, d_ids, d_ylt, ld, n, ctx->C, ctx->d_err,
@@ -236,39 +272,25 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                       nullptr};
     // Map mode 2 (direct rows behind the presence bitmap): a probe of the YET's hit rate lets
     // the scan skip the bitmap test when (nearly) every id is in the store; results do not
-    // depend on it.  ARA_MAP_PROBE=0 disables the probe (tuning).
-    // The kernels read the probe on the device and run their mode-1 body when >= 99% of the
-    // sampled ids are present.  The host also reads the PREVIOUS run's probe counts (copied back
-    // asynchronously, never waited for): when they said "present" it launches the plain mode-1
-    // kernel, which is ~3% faster than the combined one (a perf heuristic only: every mode gives
-    // the same YLT, so a stale verdict is never wrong).
-    const bool hoist = (flags & ARA_RUN_HOIST) && !extra;
-    const bool hoist_bm = hoist && ctx->store.d_oc_bitmap;
-    bool mode1 = false;
-    if (!extra && ctx->probe && (ctx->store.map_mode == 2 || hoist_bm)) {
-        if (ctx->probe_pending) {
-            const cudaError_t q = cudaEventQuery(ctx->ev_probe);
-            if (q == cudaSuccess) {
-                const unsigned long long hit = ctx->h_probe[0], cnt = ctx->h_probe[1];
-                ctx->probe_mode1 = cnt > 0 && 100ull * hit >= 99ull * cnt;
-                ctx->probe_pending = false;
-            } else if (q == cudaErrorNotReady) {
-                cudaGetLastError();  // "not ready" is not an error; keep it out of the launch checks
-            } else {
-                return cuda_fail(ctx, q, "hit probe event");
-            }
-        }
-        mode1 = ctx->probe_mode1;
+    // depend on it.  ARA_MAP_PROBE=0 disables the probe (tuning).  The kernels read the probe
+    // on the device and run their mode-1 body when >= 99% of the sampled ids are present; when
+    // the previous run's probe said the same, the host launches the plain mode-1 kernel (~3%
+    // faster than the combined one).
+    const bool mode1 = probing && ctx->probe_mode1;
+    if (probing) {
         cudaError_t pe = ara::launch_hit_probe(d_off, d_ids, n, ctx->store.d_map, ctx->C,
                                                ctx->d_probe, ctx->stream, &ctx->launches);
-        if (pe == cudaSuccess && !ctx->probe_pending) {
-            pe = cudaMemcpyAsync(ctx->h_probe, ctx->d_probe, 16, cudaMemcpyDeviceToHost,
-                                 ctx->stream);
-            if (pe == cudaSuccess) pe = cudaEventRecord(ctx->ev_probe, ctx->stream);
-            ctx->probe_pending = pe == cudaSuccess;
-        }
         if (pe != cudaSuccess) return cuda_fail(ctx, pe, "hit probe");
         s.probe = ctx->d_probe;
+    }
+    if (balance) {  // mark the length verdict as measured ([3] = 1) via a 1-value memset
+        ARA_CUDA(ctx, cudaMemsetAsync((char *)(ctx->d_probe + 3), 1, 1, ctx->stream));
+    }
+    if (!ctx->probe_pending && (probing || balance)) {
+        ARA_CUDA(ctx, cudaMemcpyAsync(ctx->h_probe, ctx->d_probe, 32, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        ARA_CUDA(ctx, cudaEventRecord(ctx->ev_probe, ctx->stream));
+        ctx->probe_pending = true;
     }
     cudaError_t e;
     if (mode1) {  // a store view addressed like map mode 1 (same buffers)
@@ -529,9 +551,9 @@ ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
     if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, 4);
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_ticket, 16);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_ticket, 0, 16);
-    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_probe, 16);
-    if (e == cudaSuccess) e = cudaMemset(ctx->d_probe, 0, 16);
-    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_probe, 16);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_probe, 32);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_probe, 0, 32);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_probe, 32);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_probe, cudaEventDisableTiming);
     if (const char *sc = getenv("ARA_SCAN_SCHED"))
         ctx->sched = strcmp(sc, "static") == 0 ? 1 : strcmp(sc, "dynamic") == 0 ? 2 : 0;

@@ -176,8 +176,14 @@ struct SortScratch {
     size_t bytes = 0;
     const uint32_t *perm = nullptr;  // result of the last sort (inside d_buf)
 };
+// The sort also raises *differ when trial lengths are not all equal; launch_length_check does
+// that check alone (when the sort is skipped).
 cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch &sc, int sm_count,
-                               cudaStream_t stream, uint64_t *launches);
+                               cudaStream_t stream, uint64_t *launches,
+                               unsigned long long *differ);
+cudaError_t launch_length_check(const uint64_t *offsets, uint64_t n, SortScratch &sc,
+                                unsigned long long *differ, int sm_count, cudaStream_t stream,
+                                uint64_t *launches);
 
 // scan.cu
 // Map modes >= 1: expand the dense rows to rows by catalogue id (direct[id] = dense[map[id]]) and
@@ -197,7 +203,7 @@ cudaError_t launch_portfolio(const UnionStore &us, const uint32_t *d_map, int ma
                              cudaStream_t stream, uint64_t *launches);
 // Map mode 2: sample up to kProbeSamples of the YET's event ids (evenly strided) and count how
 // many are in the store (probe[0]) of how many sampled (probe[1]); the scans skip their
-// presence-bitmap test when at least 99% are (probe_use_bitmap).
+// presence-bitmap test when at least 99% are (probe_use_bitmap).  probe[] must be zeroed first.
 constexpr uint32_t kProbeSamples = 65536;
 cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
                              const uint32_t *d_map, uint32_t C, unsigned long long *probe,

@@ -366,15 +366,21 @@ __global__ void __launch_bounds__(256) hit_probe_kernel(const uint64_t *__restri
 }
 
 // Keys for the length sort: trial lengths (saturated to 32 bits) and trial indices.
+// Also raises *differ when some trial's length differs from trial 0's (keys == nullptr: the
+// check alone plus the identity order, used when the sort is skipped).
 __global__ void length_keys_kernel(const uint64_t *__restrict__ offsets, uint64_t n,
-                                   uint32_t *keys, uint32_t *idx)
+                                   uint32_t *keys, uint32_t *idx, unsigned long long *differ)
 {
+    const uint64_t len0 = offsets[1] - offsets[0];
+    bool d = false;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t len = offsets[t + 1] - offsets[t];
-        keys[t] = len > 0xffffffffull ? 0xffffffffu : (uint32_t)len;
+        d |= len != len0;
+        if (keys) keys[t] = len > 0xffffffffull ? 0xffffffffu : (uint32_t)len;
         idx[t] = (uint32_t)t;
     }
+    if (differ && __any_sync(0xffffffffu, d) && (threadIdx.x & 31u) == 0) atomicOr(differ, 1ull);
 }
 
 template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D>
@@ -551,32 +557,31 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
     const ScanShape sh = scan_shape_for_width(st.width, st.group_override);
     switch (sh.G * 16 + sh.CH) {
         case 1 * 16 + 1: return launch_gc<1, 1>(st, s, sm_count, stream);
-        case 2 * 16 + 1: return launch_gc<2, 1>(st, s, sm_count, stream);
+        case 2 * 16 + 1: return launch_gc<2, 1, 4>(st, s, sm_count, stream);
         case 4 * 16 + 1:  // W = 16 with G = 4 (tuning)
             switch (st.min_blocks) {
                 case 5: return launch_gc<4, 1, 5>(st, s, sm_count, stream);
                 case 6: return launch_gc<4, 1, 6>(st, s, sm_count, stream);
                 default: return launch_gc<4, 1>(st, s, sm_count, stream);
             }
-        case 4 * 16 + 2: return launch_gc<4, 2>(st, s, sm_count, stream);
+        case 4 * 16 + 2: return launch_gc<4, 2, 3>(st, s, sm_count, stream);
         case 4 * 16 + 3: return launch_gc<4, 3>(st, s, sm_count, stream);
         case 4 * 16 + 4: return launch_gc<4, 4>(st, s, sm_count, stream);
         case 2 * 16 + 2:  // W = 16 (default)
             switch (st.min_blocks) {
                 case 4: return launch_gc<2, 2, 4>(st, s, sm_count, stream);
-                default: return launch_gc<2, 2>(st, s, sm_count, stream);
+                default: return launch_gc<2, 2, 3>(st, s, sm_count, stream);
             }
         case 1 * 16 + 4: return launch_gc<1, 4>(st, s, sm_count, stream);  // W = 16, G = 1
         default: --*launches; return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch &sc, int sm_count,
-                               cudaStream_t stream, uint64_t *launches)
+namespace {
+// Scratch of the length sort / check: keys, indices (in/out), CUB temporary storage.
+cudaError_t sort_scratch(uint64_t n, SortScratch &sc, size_t &temp, cudaStream_t stream)
 {
-    if (n == 0) return cudaSuccess;
-    if (n > 0xffffffffull) return cudaErrorInvalidValue;
-    size_t temp = 0;
+    temp = 0;
     cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(
         nullptr, temp, (const uint32_t *)nullptr, (uint32_t *)nullptr, (const uint32_t *)nullptr,
         (uint32_t *)nullptr, (int)n, 0, 32, stream);
@@ -590,11 +595,39 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
         if (e != cudaSuccess) return e;
         sc.bytes = need;
     }
+    return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t launch_length_check(const uint64_t *offsets, uint64_t n, SortScratch &sc,
+                                unsigned long long *differ, int sm_count, cudaStream_t stream,
+                                uint64_t *launches)
+{
+    if (n == 0) return cudaSuccess;
+    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    size_t temp;
+    cudaError_t e = sort_scratch(n, sc, temp, stream);
+    if (e != cudaSuccess) return e;
+    uint32_t *idx = (uint32_t *)sc.d_buf + 2 * n;  // identity order (trials equally long)
+    ++*launches;
+    length_keys_kernel<<<sm_count * 4, 256, 0, stream>>>(offsets, n, nullptr, idx, differ);
+    sc.perm = idx;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch &sc, int sm_count,
+                               cudaStream_t stream, uint64_t *launches, unsigned long long *differ)
+{
+    if (n == 0) return cudaSuccess;
+    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    size_t temp;
+    cudaError_t e = sort_scratch(n, sc, temp, stream);
+    if (e != cudaSuccess) return e;
     uint32_t *keys_in = (uint32_t *)sc.d_buf, *keys_out = keys_in + n;
     uint32_t *idx_in = keys_out + n, *idx_out = idx_in + n;
     void *tmp = (void *)(((uintptr_t)(idx_out + n) + 255) & ~(uintptr_t)255);
     ++*launches;
-    length_keys_kernel<<<sm_count * 4, 256, 0, stream>>>(offsets, n, keys_in, idx_in);
+    length_keys_kernel<<<sm_count * 4, 256, 0, stream>>>(offsets, n, keys_in, idx_in, differ);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     ++*launches;  // the CUB radix sort (a few internal kernels)
@@ -609,8 +642,6 @@ cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint6
                              cudaStream_t stream, uint64_t *launches)
 {
     if (n_trials == 0) return cudaSuccess;
-    cudaError_t e = cudaMemsetAsync(probe, 0, 16, stream);
-    if (e != cudaSuccess) return e;
     ++*launches;
     hit_probe_kernel<<<kProbeSamples / 256, 256, 0, stream>>>(offsets, ids, n_trials, d_map, C,
                                                                probe);
