@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ara_internal.h"
 
@@ -102,10 +103,13 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
                 for (uint32_t u = 0; u < nu; ++u)
                     if ((key & mask) == s_uprefix[u]) slot = u * kBins + ((key >> shift) & 0xff);
             }
-            // warp-aggregated histogram update: one atomic per distinct slot in the warp
-            const uint32_t peers = __match_any_sync(0xffffffffu, slot);
-            if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(&sh[0][0] + slot, (uint32_t)__popc(peers));
+            // warp-aggregated histogram update: one atomic per distinct slot in the warp (after
+            // the first passes most warps hold no element of any surviving prefix: skip them)
+            if (__any_sync(0xffffffffu, slot != 0xffffffffu)) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+                if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                    atomicAdd(&sh[0][0] + slot, (uint32_t)__popc(peers));
+            }
         }
         __syncthreads();
         uint32_t *gh = P.hist + (size_t)pass * ARA_MAX_P * kBins;
@@ -227,7 +231,10 @@ cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const 
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
         if (!coop || occ < 1) return cudaErrorNotSupported;
-        scratch.grid = sm_count * (occ < 2 ? occ : 2);
+        int per_sm = 4;  // blocks per SM (tuning: ARA_METRICS_BLOCKS_PER_SM; 4 measured best)
+        if (const char *b = getenv("ARA_METRICS_BLOCKS_PER_SM")) per_sm = atoi(b);
+        if (per_sm < 1) per_sm = 1;
+        scratch.grid = sm_count * (occ < per_sm ? occ : per_sm);
         scratch.bytes = (size_t)kPasses * ARA_MAX_P * kBins * 4 +
                         (size_t)scratch.grid * ARA_MAX_P * 16 + 2 * ARA_MAX_P * 8;
         e = cudaMalloc(&scratch.d_buf, scratch.bytes);

@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -39,3 +41,28 @@ def test_partition_matches_dist():
     from paper_1308_2572_b200.dist import partition_trials
     for n, R in ((1_000_000, 8), (10, 4), (7, 3)):
         assert [bench.partition(n, r, R) for r in range(R)] == partition_trials(n, R)
+
+
+@pytest.mark.gpu
+def test_bench_json_line_on_gpu():
+    """bench.py on the GPU (medium config, short run) prints one JSON line with every key the
+    driver reads, a positive value, the roofline / e2e / clocks objects and kernel launches."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "medium",
+                          "--steps", "3", "--warmup", "3", "--e2e-steps", "2"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "gpu_launches", "clocks", "e2e", "cpu_baseline"):
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3 and d["dtype"] == "f64"
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["gpu_launches"] >= 3 * 3  # probe / length check or sort, scan, metrics per step
+    assert d["e2e"]["h2d_bytes_per_step"] > 4 * 10**8 and d["e2e"]["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert "sm_mhz" in d["clocks"]

@@ -34,7 +34,9 @@ def main():
             ctx.ara_metrics(d, P)
         b.record(stream)
         torch.cuda.synchronize()
-        print(json.dumps({"n": n, "ms_per_call": a.elapsed_time(b) / 20}), flush=True)
+        print(json.dumps({"n": n, "ms_per_call": a.elapsed_time(b) / 20,
+                          "blocks_per_sm": os.environ.get("ARA_METRICS_BLOCKS_PER_SM", "2")}),
+              flush=True)
     ctx.close()
 
 
