@@ -137,10 +137,10 @@ def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0):
     threads = max(1, len(os.sched_getaffinity(0)))
     k = (spec.k_min + spec.k_max) // 2
 
-    def run(n_tr):
+    def run(n_tr, nt=threads):
         off, ev = datagen.generate_yet(spec, ds_host_elts.pool, 0, n_tr)
         t0 = time.perf_counter()
-        oracle.run_analysis(ds_host_elts, n_threads=threads, trial_offsets=off, events=ev)
+        oracle.run_analysis(ds_host_elts, n_threads=nt, trial_offsets=off, events=ev)
         return time.perf_counter() - t0, int(off[-1])
 
     t_build, _ = run(1)
@@ -156,7 +156,13 @@ def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0):
         t, n_ev = run(n_tr)
     work = max(t - t_build, 1e-9)
     value = n_ev * spec.n_layers / work
+    # one thread on a ~2 s slice: the per-core rate (the paper's sequential C++ did
+    # 2.96e6 trial-events/s on one i7-2600 core)
+    n1 = max(1, min(spec.n_trials, int(2.0 * value / threads / max(1, k * spec.n_layers))))
+    t1, n_ev1 = run(n1, 1)
+    per_core = n_ev1 * spec.n_layers / max(t1 - t_build, 1e-9)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "per_core_value": per_core,
             "sample": f"first {n_tr} trials x {k} events of the {spec.name} workload "
                       f"({n_ev * spec.n_layers} trial-events, {spec.n_layers} layer(s)); "
                       f"oracle/oracle.c with {threads} threads: {t:.1f} s, minus {t_build:.2f} s "
