@@ -362,6 +362,21 @@ def main():
         except Exception:
             pass
 
+    # Secondary (arithmetic) roofline of the full fp64 scan: the algorithmic fp64 operations per
+    # trial-event -- per (event, ELT) multiply, subtract, max, min and the ELT-sum add (5E), then
+    # occurrence terms (3), running sum (1), aggregate terms (3), difference (1), trial sum (1)
+    # -- against the fp64 lane-op peak: 148 SMs x 64 fp64 lanes per clock (ncu
+    # sm__sass_thread_inst_executed_op_dfma_pred_on peak_sustained) x the SM clock.  sm_100a has no
+    # fp64 min/max instruction, so the kernel issues each max/min as a DSETP (fp64 pipe) + 2 FSEL.
+    alu = None
+    if args.precision == 64 and not args.hoist:
+        ops = (5 * E + 9) * n_ev * L
+        alu_peak = 148 * 64 * 1.965e9
+        alu = {"unit": "fp64 lane-ops/s", "ops_per_trial_event": 5 * E + 9,
+               "achieved": ops / (scan_ms * 1e-3), "peak": alu_peak,
+               "frac": ops / (scan_ms * 1e-3) / alu_peak,
+               "peak_source": "148 SMs x 64 fp64 lanes/clk (ncu peak_sustained) x 1965 MHz"}
+
     # ---- end to end through the host-buffer C-ABI call
     e2e = None
     if not args.no_e2e:
@@ -426,7 +441,7 @@ def main():
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                          "bytes_model": bytes_model,
-                         "physical": physical},
+                         "physical": physical, "alu": alu},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
