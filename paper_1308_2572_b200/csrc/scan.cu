@@ -512,6 +512,8 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
                         return launch_gc<4, 1, 4, false, double, true, 4>(st, s, sm_count, stream);
                     return launch_gc<4, 1, 3, false, double, true, 4>(st, s, sm_count, stream);
                 }
+                if (st.depth == 4 && st.min_blocks == 3)
+                    return launch_gc<2, 2, 3, false, double, true, 4>(st, s, sm_count, stream);
                 if (st.depth == 4)
                     return launch_gc<2, 2, 2, false, double, true, 4>(st, s, sm_count, stream);
                 if (st.min_blocks == 2)
