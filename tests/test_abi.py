@@ -89,3 +89,37 @@ def test_binding_structs_match_header_layout(tmp_path, cname, pyname):
     got = [int(x) for x in subprocess.check_output([str(exe)], text=True).split()]
     assert got[0] == ctypes.sizeof(st)
     assert got[1:] == [getattr(st, f).offset for f in fields]
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    exe = tmp_path / "ara_example"
+    pkg = os.path.join(ROOT, "paper_1308_2572_b200")
+    build.build()
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I",
+                           os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "ara_example.c"), "-L", pkg, "-lara",
+                           f"-Wl,-rpath,{pkg}", "-o", str(exe)])
+    return exe
+
+
+def test_c_example_links_and_fails_loudly_without_gpu(tmp_path):
+    """examples/ara_example.c compiles against include/ara.h alone and links libara.so; without a
+    GPU ara_create reports ARA_ERR_CUDA (no CPU fallback)."""
+    import subprocess
+    import torch
+    exe = _build_c_example(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: see test_c_example_on_gpu")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 1 and "ARA_ERR_CUDA" in r.stderr
+
+
+@pytest.mark.gpu
+def test_c_example_on_gpu(tmp_path):
+    """The C example on the GPU prints SPEC.md's worked-example YLT [[150, 0]] (L252-L262)."""
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "YLT 150 0" in r.stdout
