@@ -441,7 +441,11 @@ def main():
                          "kernel_ms": scan_ms,
                          "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
                          "bytes_model": bytes_model,
-                         "physical": physical, "alu": alu},
+                         "physical": physical, "alu": alu,
+                         "note": ("frac > 1 because the north-star bytes count every gathered "
+                                  "row as an HBM read: the row store is L2-resident by design "
+                                  "(see traffic = DRAM bytes per launch from ncu, and physical)")
+                                 if achieved > peak else None},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
