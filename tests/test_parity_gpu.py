@@ -761,3 +761,23 @@ def test_fuzz_parity(stream, monkeypatch, seed):
         assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx,
                                      flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST), want)
     ctx.close()
+
+
+def test_stale_run_statistics_never_change_results(stream, monkeypatch):
+    """The host reads the previous run's length / hit-probe verdicts to choose the schedule and
+    the kernel body.  Alternate YETs on one context so that every run sees a stale verdict:
+    equal-length <-> ragged trials (identity order vs length sort) and all-present <-> mostly
+    absent ids (mode-1 body vs presence bitmap) -- every YLT stays the oracle's, bit for bit."""
+    monkeypatch.setenv("ARA_MAP_MODE", "2")
+    base = datagen.PRESETS["medium"].replace(n_trials=2500, seed=3)
+    ds = datagen.generate(base, with_yet=False)
+    yets = [datagen.generate_yet(base.replace(k_min=k0, k_max=k1, hit=h), ds.pool, 0, 2500)
+            for k0, k1, h in ((64, 64, 1.0), (0, 300, 0.05), (64, 64, 0.05), (5, 200, 1.0))]
+    ctx = make_ctx(ds, stream)
+    for rep in range(2):
+        for off, ev in yets:
+            want = oracle.run_analysis(ds, n_threads=8, trial_offsets=off, events=ev)
+            for flags in (ara.ARA_RUN_SYNC, ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST):
+                assert_bit_identical(gpu_ylt(ds, stream, ctx=ctx, flags=flags, offsets=off,
+                                             events=ev), want)
+    ctx.close()
