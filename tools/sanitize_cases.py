@@ -4,7 +4,8 @@
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
 
 single layer (map modes 0-2), multi-layer per-layer rows, union rows with the shared F row and
-with register shuffles, F4 outputs, fp32, host-buffer run, PML/TVaR.  Each YLT is checked against
+with register shuffles, F4 outputs, fp32, host-buffer run, PML/TVaR, the hoisted scan, and the
+runs that follow the previous run's length / hit-probe verdicts (identity order, mode-1 body).  Each YLT is checked against
 the oracle (test infrastructure), so a run that passes under the sanitizer is also correct."""
 import os
 import sys
@@ -44,7 +45,14 @@ def main():
             inc = torch.empty((L, int(ds.trial_offsets[-1])), dtype=torch.float64, device=dev)
             ctx.ara_run_outputs(off, ev, ylt, d_max_occ=mo, d_event_inc=inc, flags=ara.ARA_RUN_SYNC)
         else:
-            ctx.ara_run(off, ev, ylt, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_VALIDATE)
+            # three runs: the later ones use the previous runs' length / hit verdicts (identity
+            # order, mode-1 body), then the hoisted scan
+            for fl in (ara.ARA_RUN_SYNC | ara.ARA_RUN_VALIDATE, ara.ARA_RUN_SYNC):
+                ctx.ara_run(off, ev, ylt, flags=fl)
+            got = ylt.cpu().numpy()
+            if L <= 8:
+                ctx.ara_run(off, ev, ylt, flags=ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST)
+                assert np.array_equal(ylt.cpu().numpy(), got), "hoisted YLT differs"
         got = ylt.cpu().numpy()
         info = ctx.ara_get_info()
         pml, tvar = ctx.ara_metrics(ylt[0], [0.9, 0.99])
@@ -58,6 +66,9 @@ def main():
         return info
 
     tiny = datagen.PRESETS["tiny"].replace(n_trials=300, k_min=0, k_max=40)
+    run(datagen.generate(tiny.replace(k_min=24, k_max=24)))  # equal lengths: identity order
+    run(datagen.generate(datagen.PRESETS["tiny"].replace(n_trials=200, k_min=16, k_max=16,
+                                                         hit=1.0)))  # all present: mode-1 body
     for mode in ("0", "1", "2"):
         run(datagen.generate(tiny), env=[("ARA_MAP_MODE", mode)])
     run(datagen.generate(tiny), outputs=True)
