@@ -211,6 +211,9 @@ def main():
                     help="ARA_RUN_HOIST: Alg. 1 lines 4-17 once per distinct event per run, then "
                          "one table read per occurrence (SURVEY.md 7 deferred exact lever; "
                          "reported separately from the full per-occurrence scan)")
+    ap.add_argument("--metrics", default="gather", choices=["gather", "sharded"],
+                    help="N > 1: gather the YLT slices and compute PML/TVaR on every rank (north "
+                         "star), or ara_metrics_sharded (histograms all-reduced per pass)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -290,6 +293,8 @@ def main():
         if timed:
             b.record(stream)
             scan_ev.append((a, b))
+        if world > 1 and args.metrics == "sharded":
+            return [adist.sharded_metrics(ctx, d_ylt_loc[l], n_total, P) for l in range(L)]
         full = gather()
         res = [ctx.ara_metrics(full[l], P) for l in range(L)]  # A9 (synchronous)
         return res
@@ -392,9 +397,13 @@ def main():
             tt = time.perf_counter()
             ctx.ara_run_host(h_off_np, ids_np, h_ylt, flags=run_flags)  # H2D YET, scan, D2H YLT
             d_ylt_loc.copy_(torch.from_numpy(h_ylt), non_blocking=False)
-            full = gather()
-            for l in range(L):
-                ctx.ara_metrics(full[l], P)
+            if world > 1 and args.metrics == "sharded":
+                for l in range(L):
+                    adist.sharded_metrics(ctx, d_ylt_loc[l], n_total, P)
+            else:
+                full = gather()
+                for l in range(L):
+                    ctx.ara_metrics(full[l], P)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - tt)
         t_e2e = statistics.median(ts)
@@ -428,7 +437,9 @@ def main():
                        "trials": n_total, "trials_per_gpu": n_loc,
                        "events_per_trial": spec.k_min,
                        "parallelism": f"trial-sharded x{world}, {args.scaling} scaling "
-                                      f"(NCCL all-gather of the YLT for PML/TVaR)"
+                                      + ("(PML/TVaR by sharded radix select, histograms "
+                                         "all-reduced per pass)" if args.metrics == "sharded"
+                                         else "(NCCL all-gather of the YLT for PML/TVaR)")
                        if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2: the 4 GB YET is streamed from HBM every "
                              "step; the ELT store (2.6 MB rows + 8 MB map) is L2-resident",

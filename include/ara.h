@@ -237,6 +237,31 @@ ara_status ara_synchronize(ara_ctx *ctx);
 ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32_t n_p,
                        const double *p, double *pml_out, double *tvar_out);
 
+/*
+ * ara_metrics_sharded -- PML / TVaR of a YLT row that is split over several processes (one
+ * contiguous slice per rank, e.g. the trial shards of SURVEY.md 8(e)), without gathering the
+ * row: the same MSB radix select as ara_metrics runs pass by pass on every rank's slice, and
+ * between passes the caller's reduction sums the per-rank 256-bin histograms; the tail sums
+ * and counts are reduced the same way.  Every rank must call it with the same n_global, n_p and
+ * p; every rank receives the same PML (exact) and TVaR (the tail sum's order differs from
+ * ara_metrics': equal within rounding).
+ *   d_ylt_slice[n_local]  device fp64, this rank's part of the row (n_local may be 0)
+ *   n_global              the whole row's length (sum of n_local over ranks), > 0
+ *   d_xbuf, xbuf_bytes    caller-owned device exchange buffer of >= ARA_MAX_P * 256 * 8 bytes
+ *   reduce(offset, count, is_f64, user): the caller's element-wise SUM across all ranks, in
+ *                         place, of `count` int64 (is_f64 = 0) or fp64 (is_f64 = 1) values at
+ *                         byte `offset` of d_xbuf, ordered after the work already enqueued on
+ *                         the context's stream and before what follows (e.g. an NCCL
+ *                         all-reduce on that stream); returns 0 on success.  Called 10 times.
+ * Synchronous.  Errors: ARA_ERR_EMPTY (n_global == 0), ARA_ERR_ARG (p outside (0,1), NULL,
+ * small buffer, n_local > n_global, the callback failed), ARA_ERR_CUDA.
+ */
+typedef int (*ara_shard_reduce)(uint64_t offset, uint64_t count, int is_f64, void *user);
+ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t n_local,
+                               uint64_t n_global, uint32_t n_p, const double *p, double *pml_out,
+                               double *tvar_out, void *d_xbuf, uint64_t xbuf_bytes,
+                               ara_shard_reduce reduce, void *user);
+
 /* ara_metrics on a HOST YLT row (copied to the device first).  Synchronous. */
 ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, uint32_t n_p,
                             const double *p, double *pml_out, double *tvar_out);

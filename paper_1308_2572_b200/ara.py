@@ -31,8 +31,14 @@ ARA_MAX_P = 32
 EXPORTS = ["ara_status_string", "ara_create", "ara_set_precision", "ara_set_stream", "ara_destroy", "ara_last_error",
            "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
            "ara_synchronize",
-           "ara_metrics", "ara_metrics_host", "ara_get_info", "ara_layer_store_shape",
+           "ara_metrics", "ara_metrics_host", "ara_metrics_sharded", "ara_get_info",
+           "ara_layer_store_shape",
            "ara_export_store"]
+
+
+# int reduce(uint64_t offset, uint64_t count, int is_f64, void *user)   (include/ara.h)
+SHARD_REDUCE = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                ctypes.c_void_p)
 
 
 class AraLibraryMissing(ImportError):
@@ -97,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "ara_synchronize": ([p], i32),
         "ara_metrics": ([p, p, u64, u32, p, p, p], i32),
         "ara_metrics_host": ([p, p, u64, u32, p, p, p], i32),
+        "ara_metrics_sharded": ([p, p, u64, u64, u32, p, p, p, p, u64, SHARD_REDUCE, p], i32),
         "ara_get_info": ([p, ctypes.POINTER(Info)], i32),
         "ara_layer_store_shape": ([p, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
         "ara_export_store": ([p, u32, p, p], i32),
@@ -153,6 +160,7 @@ class Context:
         if st != ARA_OK:
             raise AraError(st, "ara_create failed")
         self.device = device
+        self.stream = stream
 
     def _check(self, st: int):
         if st != ARA_OK:
@@ -236,6 +244,41 @@ class Context:
         self._check(lib().ara_metrics(self._ptr, _dptr(d_ylt_row, "torch.float64"),
                                       d_ylt_row.numel(), pp.shape[0], _hptr(pp), _hptr(pml),
                                       _hptr(tvar)))
+        return pml, tvar
+
+    def ara_metrics_sharded(self, d_ylt_slice, n_global: int, p: Sequence[float], allreduce):
+        """PML / TVaR of a YLT row split over ranks (this rank's slice on the device).
+        ``allreduce(tensor)`` must sum a CUDA tensor in place across all ranks (e.g.
+        ``torch.distributed.all_reduce``); it is called on this context's stream."""
+        import torch
+        pp = np.ascontiguousarray(p, dtype=np.float64)
+        pml = np.empty(pp.shape[0]); tvar = np.empty(pp.shape[0])
+        dev = d_ylt_slice.device if d_ylt_slice.is_cuda else torch.device("cuda", self.device)
+        xbuf = torch.zeros(ARA_MAX_P * 256, dtype=torch.int64, device=dev)
+        err = []
+
+        def cb(offset, count, is_f64, user):
+            try:
+                view = xbuf.view(torch.uint8)[offset: offset + 8 * count]
+                view = view.view(torch.float64 if is_f64 else torch.int64)
+                if self.stream is not None:
+                    with torch.cuda.stream(self.stream):
+                        allreduce(view)
+                else:
+                    allreduce(view)
+                return 0
+            except Exception as exc:  # reported as ARA_ERR_ARG by the library
+                err.append(exc)
+                return 1
+
+        fn = SHARD_REDUCE(cb)
+        st = lib().ara_metrics_sharded(self._ptr, _dptr(d_ylt_slice, "torch.float64") if
+                                       d_ylt_slice.numel() else None, d_ylt_slice.numel(),
+                                       int(n_global), pp.shape[0], _hptr(pp), _hptr(pml),
+                                       _hptr(tvar), xbuf.data_ptr(), xbuf.numel() * 8, fn, None)
+        if err:
+            raise err[0]
+        self._check(st)
         return pml, tvar
 
     def ara_metrics_host(self, h_ylt_row, p: Sequence[float]):

@@ -608,6 +608,7 @@ void ara_destroy(ara_ctx *ctx)
     if (ctx->ev_probe) cudaEventDestroy(ctx->ev_probe);
     cudaFreeHost(ctx->h_err);
     cudaFree(ctx->metrics.d_buf);
+    cudaFree(ctx->metrics.d_shard);
     cudaFree(ctx->sort.d_buf);
     for (int i = 0; i < 2; ++i) {
         cudaFree(ctx->d_ids_stage[i]);
@@ -960,6 +961,31 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
                                             ctx->sm_count, ctx->device, ctx->stream,
                                             &ctx->launches);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");
+        return ARA_OK;
+    });
+}
+
+ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t n_local,
+                               uint64_t n_global, uint32_t n_p, const double *p, double *pml_out,
+                               double *tvar_out, void *d_xbuf, uint64_t xbuf_bytes,
+                               ara_shard_reduce reduce, void *user)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (n_global == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
+        ara_status s = validate_p(ctx, n_p, p);
+        if (s != ARA_OK) return s;
+        if ((n_local && !d_ylt_slice) || !pml_out || !tvar_out || !d_xbuf || !reduce)
+            return fail(ctx, ARA_ERR_ARG, "NULL pointer");
+        if (n_local > n_global) return fail(ctx, ARA_ERR_ARG, "n_local > n_global");
+        if (xbuf_bytes < (uint64_t)ARA_MAX_P * 256 * 8)
+            return fail(ctx, ARA_ERR_ARG, "exchange buffer smaller than %d bytes",
+                        ARA_MAX_P * 256 * 8);
+        cudaError_t e = ara::launch_metrics_sharded(
+            d_ylt_slice, n_local, n_global, n_p, p, pml_out, tvar_out, (char *)d_xbuf,
+            (ara::ShardReduce)reduce, user, ctx->metrics, ctx->sm_count, ctx->stream,
+            &ctx->launches);
+        if (e == cudaErrorUnknown) return fail(ctx, ARA_ERR_ARG, "the reduction callback failed");
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "sharded metrics");
         return ARA_OK;
     });
 }

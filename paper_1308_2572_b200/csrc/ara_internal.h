@@ -217,7 +217,18 @@ struct MetricsScratch {
     void *d_buf = nullptr;
     size_t bytes = 0;
     int grid = 0;
+    void *d_shard = nullptr;  // sharded metrics: state + per-block tail partials
+    size_t shard_bytes = 0;
 };
+// Caller-supplied reduction for the sharded metrics: element-wise SUM across all ranks, in
+// place, of `count` values (int64 if !is_f64, else fp64) at byte offset `offset` of the caller's
+// device exchange buffer, ordered on the context's stream.  Returns 0 on success.
+typedef int (*ShardReduce)(uint64_t offset, uint64_t count, int is_f64, void *user);
+cudaError_t launch_metrics_sharded(const double *d_slice, uint64_t n_local, uint64_t n_global,
+                                   uint32_t n_p, const double *p, double *pml_out,
+                                   double *tvar_out, char *d_xbuf, ShardReduce reduce,
+                                   void *user, MetricsScratch &scratch, int sm_count,
+                                   cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
                            double *pml_out, double *tvar_out, MetricsScratch &scratch,
                            int sm_count, int device, cudaStream_t stream, uint64_t *launches);

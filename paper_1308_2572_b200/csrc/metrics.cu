@@ -8,6 +8,9 @@
 // elements still matching that probability's key prefix), then sums the tails.  Partial
 // tail sums are combined in block order, so the result is deterministic for a given grid.
 #include <cooperative_groups.h>
+#include <string.h>
+
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -217,6 +220,185 @@ __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Sharded PML/TVaR (launch_metrics_sharded): the YLT row is split over ranks; the same MSB radix
+// select runs as separate per-pass kernels, and between passes the caller's reduction sums the
+// per-rank histograms (a real exchange step: 8 x n_p x 256 counts instead of gathering the
+// row).  Every rank holds identical state after each reduction, so the distinct-prefix
+// numbering -- and with it the histogram layout -- agrees across ranks.
+struct ShardState {
+    unsigned long long prefix[ARA_MAX_P];  // key prefix found so far, per probability
+    unsigned long long rank[ARA_MAX_P];    // global rank within that prefix
+};
+
+// distinct prefixes (under mask) of the probabilities, in first-appearance order
+__device__ __forceinline__ uint32_t distinct_prefixes(const ShardState &S, uint32_t n_p,
+                                                      uint64_t mask, uint64_t *uprefix,
+                                                      uint32_t *uof)
+{
+    uint32_t nu = 0;
+    for (uint32_t i = 0; i < n_p; ++i) {
+        uint32_t u = 0;
+        while (u < nu && uprefix[u] != (S.prefix[i] & mask)) ++u;
+        if (u == nu) uprefix[nu++] = S.prefix[i] & mask;
+        uof[i] = u;
+    }
+    return nu;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    shard_hist_kernel(const double *__restrict__ v, uint64_t n, uint32_t n_p, int pass,
+                      const ShardState *__restrict__ st, long long *__restrict__ hist)
+{
+    __shared__ uint32_t sh[ARA_MAX_P * kBins];
+    __shared__ uint64_t s_uprefix[ARA_MAX_P];
+    __shared__ uint32_t s_uof[ARA_MAX_P];
+    __shared__ uint32_t s_nu;
+    const int shift = 56 - 8 * pass;
+    const uint64_t mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+    if (threadIdx.x == 0) s_nu = distinct_prefixes(*st, n_p, mask, s_uprefix, s_uof);
+    for (uint32_t i = threadIdx.x; i < ARA_MAX_P * kBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint32_t nu = s_nu, lane = threadIdx.x & 31u;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x - lane; e0 < n;
+         e0 += stride) {  // warp-uniform trip count
+        const uint64_t e = e0 + lane;
+        uint32_t slot = 0xffffffffu;
+        if (e < n) {
+            const uint64_t key = to_key(v[e]);
+            for (uint32_t u = 0; u < nu; ++u)
+                if ((key & mask) == s_uprefix[u]) slot = u * kBins + ((key >> shift) & 0xff);
+        }
+        if (__any_sync(0xffffffffu, slot != 0xffffffffu)) {
+            const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+            if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(sh + slot, (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nu * kBins; i += blockDim.x)
+        if (sh[i]) atomicAdd((unsigned long long *)(hist + i), (unsigned long long)sh[i]);
+}
+
+// One block: every probability finds the bin of the (globally reduced) histogram that holds its
+// rank and extends its prefix by that digit.
+__global__ void __launch_bounds__(kThreads)
+    shard_select_kernel(uint32_t n_p, int pass, ShardState *st, const long long *__restrict__ hist)
+{
+    __shared__ uint64_t s_uprefix[ARA_MAX_P];
+    __shared__ uint32_t s_uof[ARA_MAX_P];
+    __shared__ uint32_t s_nu;
+    __shared__ unsigned long long s_wsum[kThreads / 32];
+    __shared__ unsigned long long s_prefix_n[ARA_MAX_P], s_rank_n[ARA_MAX_P];
+    const int shift = 56 - 8 * pass;
+    const uint64_t mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
+    if (threadIdx.x == 0) s_nu = distinct_prefixes(*st, n_p, mask, s_uprefix, s_uof);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    static_assert(kThreads == kBins, "one bin per thread");
+    for (uint32_t u = 0; u < s_nu; ++u) {
+        const unsigned long long cnt = (unsigned long long)hist[u * kBins + threadIdx.x];
+        unsigned long long incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) s_wsum[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        unsigned long long before = 0;
+        for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) before += s_wsum[w];
+        incl += before;
+        const unsigned long long excl = incl - cnt;
+        for (uint32_t i = 0; i < n_p; ++i) {
+            const unsigned long long r = st->rank[i];
+            if (s_uof[i] == u && r >= excl && r < incl) {
+                s_prefix_n[i] = st->prefix[i] | ((unsigned long long)threadIdx.x << shift);
+                s_rank_n[i] = r - excl;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < n_p) {
+        st->prefix[threadIdx.x] = s_prefix_n[threadIdx.x];
+        st->rank[threadIdx.x] = s_rank_n[threadIdx.x];
+    }
+}
+
+// Tail sums of (v - PML) over v >= PML for each distinct PML, per block, then combined in block
+// order by shard_tail_combine_kernel: deterministic for a given grid.
+__global__ void __launch_bounds__(kThreads)
+    shard_tail_kernel(const double *__restrict__ v, uint64_t n, uint32_t n_p,
+                      const ShardState *__restrict__ st, double *part_sum,
+                      unsigned long long *part_cnt)
+{
+    __shared__ uint64_t s_uprefix[ARA_MAX_P];
+    __shared__ uint32_t s_uof[ARA_MAX_P];
+    __shared__ uint32_t s_nu;
+    __shared__ double s_red[kThreads / 32];
+    __shared__ unsigned long long s_redc[kThreads / 32];
+    if (threadIdx.x == 0) s_nu = distinct_prefixes(*st, n_p, ~0ull, s_uprefix, s_uof);
+    __syncthreads();
+    const uint64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = (uint64_t)blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t u = 0; u < s_nu; ++u) {
+        const uint64_t q = s_uprefix[u];
+        const double qv = from_key(q);
+        double sum = 0.0;
+        unsigned long long c = 0;
+        for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+            const double x = v[e];
+            if (to_key(x) >= q) {
+                sum += x - qv;
+                ++c;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sum += __shfl_down_sync(0xffffffffu, sum, o);
+            c += __shfl_down_sync(0xffffffffu, c, o);
+        }
+        if (lane == 0) {
+            s_red[warp] = sum;
+            s_redc[warp] = c;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double bs = 0.0;
+            unsigned long long bc = 0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                bs += s_red[w];
+                bc += s_redc[w];
+            }
+            part_sum[(size_t)blockIdx.x * ARA_MAX_P + u] = bs;
+            part_cnt[(size_t)blockIdx.x * ARA_MAX_P + u] = bc;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void shard_tail_combine_kernel(uint32_t n_p, int blocks, const ShardState *st,
+                                          const double *part_sum,
+                                          const unsigned long long *part_cnt, double *sum_out,
+                                          long long *cnt_out)
+{
+    __shared__ uint64_t s_uprefix[ARA_MAX_P];
+    __shared__ uint32_t s_uof[ARA_MAX_P];
+    if (threadIdx.x == 0) distinct_prefixes(*st, n_p, ~0ull, s_uprefix, s_uof);
+    __syncthreads();
+    if (threadIdx.x < n_p) {
+        const uint32_t u = s_uof[threadIdx.x];
+        double sum = 0.0;
+        unsigned long long c = 0;
+        for (int b = 0; b < blocks; ++b) {
+            sum += part_sum[(size_t)b * ARA_MAX_P + u];
+            c += part_cnt[(size_t)b * ARA_MAX_P + u];
+        }
+        sum_out[threadIdx.x] = sum;
+        cnt_out[threadIdx.x] = (long long)c;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
@@ -274,6 +456,84 @@ cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const 
     for (uint32_t i = 0; i < n_p; ++i) {
         pml_out[i] = host[i];
         tvar_out[i] = host[n_p + i];
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_metrics_sharded(const double *d_slice, uint64_t n_local, uint64_t n_global,
+                                   uint32_t n_p, const double *p, double *pml_out,
+                                   double *tvar_out, char *d_xbuf, ShardReduce reduce,
+                                   void *user, MetricsScratch &scratch, int sm_count,
+                                   cudaStream_t stream, uint64_t *launches)
+{
+    // scratch: the shard state and the per-block tail partials (the cooperative kernel's buffer
+    // is large enough: kPasses x ARA_MAX_P x kBins x 4 bytes)
+    cudaError_t e;
+    const int blocks = sm_count * 4;
+    const size_t need = sizeof(ShardState) + (size_t)blocks * ARA_MAX_P * 16;
+    if (scratch.shard_bytes < need) {
+        cudaFree(scratch.d_shard);
+        scratch.d_shard = nullptr;
+        scratch.shard_bytes = 0;
+        e = cudaMalloc(&scratch.d_shard, need);
+        if (e != cudaSuccess) return e;
+        scratch.shard_bytes = need;
+    }
+    ShardState h{};
+    for (uint32_t i = 0; i < n_p; ++i) {
+        uint64_t r = (uint64_t)ceil(p[i] * (double)n_global);  // nearest rank, fp64 (R11)
+        if (r < 1) r = 1;
+        if (r > n_global) r = n_global;
+        h.rank[i] = r - 1;
+    }
+    ShardState *st = (ShardState *)scratch.d_shard;
+    double *part_sum = (double *)((char *)scratch.d_shard + sizeof(ShardState));
+    unsigned long long *part_cnt = (unsigned long long *)(part_sum + (size_t)blocks * ARA_MAX_P);
+    e = cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+    long long *hist = (long long *)d_xbuf;  // [ARA_MAX_P][kBins], reduced across ranks
+    const unsigned hb = n_local ? (unsigned)std::min<uint64_t>((n_local + kThreads - 1) / kThreads,
+                                                                (uint64_t)blocks)
+                                : 1u;
+    for (int pass = 0; pass < kPasses; ++pass) {
+        e = cudaMemsetAsync(hist, 0, (size_t)n_p * kBins * 8, stream);
+        if (e != cudaSuccess) return e;
+        ++*launches;
+        shard_hist_kernel<<<hb, kThreads, 0, stream>>>(d_slice, n_local, n_p, pass, st, hist);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (reduce(0, (uint64_t)n_p * kBins, 0, user) != 0) return cudaErrorUnknown;
+        ++*launches;
+        shard_select_kernel<<<1, kThreads, 0, stream>>>(n_p, pass, st, hist);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    // tails: per-rank sums of (v - PML) and counts, reduced across ranks
+    double *sums = (double *)d_xbuf;                      // [n_p] f64
+    long long *cnts = (long long *)(d_xbuf + 8 * ARA_MAX_P);  // [n_p] i64
+    ++*launches;
+    shard_tail_kernel<<<hb, kThreads, 0, stream>>>(d_slice, n_local, n_p, st, part_sum, part_cnt);
+    ++*launches;
+    shard_tail_combine_kernel<<<1, 32, 0, stream>>>(n_p, (int)hb, st, part_sum, part_cnt, sums,
+                                                    cnts);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (reduce(0, n_p, 1, user) != 0) return cudaErrorUnknown;
+    if (reduce(8 * ARA_MAX_P, n_p, 0, user) != 0) return cudaErrorUnknown;
+    double hs[ARA_MAX_P];
+    long long hc[ARA_MAX_P];
+    e = cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs, sums, 8 * n_p, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc, cnts, 8 * n_p, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return e;
+    for (uint32_t i = 0; i < n_p; ++i) {
+        uint64_t k = h.prefix[i];
+        const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        double q;
+        memcpy(&q, &b, 8);
+        pml_out[i] = q;
+        tvar_out[i] = q + hs[i] / (double)hc[i];
     }
     return cudaSuccess;
 }

@@ -121,3 +121,20 @@ def sum_over_ranks(values: Sequence[float]):
     t = torch.tensor(list(values), dtype=torch.float64, device=_dev_for(dist))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.cpu().tolist()
+
+
+def sharded_metrics(ctx, ylt_slice, n_global: int, p):
+    """PML / TVaR of the YLT row whose slices the ranks hold, without gathering it
+    (``ara_metrics_sharded``: the radix-select histograms and tail sums are summed across ranks
+    pass by pass -- NCCL all-reduce on the context's stream; gloo stages through the host)."""
+    import torch.distributed as dist
+
+    def allreduce(t):
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(t)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h)
+            t.copy_(h)
+
+    return ctx.ara_metrics_sharded(ylt_slice, n_global, p, allreduce)
