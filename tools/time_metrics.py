@@ -35,7 +35,18 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         print(json.dumps({"n": n, "ms_per_call": a.elapsed_time(b) / 20,
-                          "blocks_per_sm": os.environ.get("ARA_METRICS_BLOCKS_PER_SM", "2")}),
+                          "blocks_per_sm": os.environ.get("ARA_METRICS_BLOCKS_PER_SM", "4")}),
+              flush=True)
+        # the sharded select on one rank (the reduction is a no-op): its local cost per call
+        import time as _t
+        for _ in range(2):
+            ctx.ara_metrics_sharded(d, n, P, lambda t: None)
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        for _ in range(10):
+            ctx.ara_metrics_sharded(d, n, P, lambda t: None)
+        torch.cuda.synchronize()
+        print(json.dumps({"n": n, "sharded_ms_per_call_1rank": (_t.perf_counter() - t0) * 100}),
               flush=True)
     ctx.close()
 
