@@ -61,25 +61,27 @@ __global__ void __launch_bounds__(256) hoist_oc_kernel(const R *__restrict__ row
     }
 }
 
-// The LP values of one table row (LP * sizeof(R) bytes, aligned to that size).
+// The LP values of one table row (LP * sizeof(R) bytes, aligned to that size).  Up to 16 bytes
+// the loads allocate in L1 (the table's hot sectors partly fit: headline 4.16 -> 3.81 ms,
+// profiles/r1_tune_hoist_l1.jsonl); 32/64-byte rows use the scan's L1-bypassing 256-bit loads.
 template <int LP, typename R>
 __device__ __forceinline__ void load_oc(const R *p, R (&v)[LP])
 {
     constexpr int B = LP * (int)sizeof(R);
     if constexpr (B == 4) {
-        asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(*(float *)&v[0]) : "l"(p));
+        asm("ld.global.nc.f32 %0, [%1];" : "=f"(*(float *)&v[0]) : "l"(p));
     } else if constexpr (B == 8) {
         if constexpr (sizeof(R) == 8)
-            asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(*(double *)&v[0]) : "l"(p));
+            asm("ld.global.nc.f64 %0, [%1];" : "=d"(*(double *)&v[0]) : "l"(p));
         else
-            asm("ld.global.nc.L1::no_allocate.v2.f32 {%0,%1}, [%2];"
+            asm("ld.global.nc.v2.f32 {%0,%1}, [%2];"
                 : "=f"(*(float *)&v[0]), "=f"(*(float *)&v[1]) : "l"(p));
     } else if constexpr (B == 16) {
         if constexpr (sizeof(R) == 8)
-            asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+            asm("ld.global.nc.v2.f64 {%0,%1}, [%2];"
                 : "=d"(*(double *)&v[0]), "=d"(*(double *)&v[1]) : "l"(p));
         else
-            asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+            asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
                 : "=f"(*(float *)&v[0]), "=f"(*(float *)&v[1]), "=f"(*(float *)&v[2]),
                   "=f"(*(float *)&v[3]) : "l"(p));
     } else {  // 32 or 64 bytes: 256-bit loads
