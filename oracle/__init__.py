@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_apply_occurrence_terms_f32.restype = f
         L.oracle_metrics.argtypes = [p, u64, u32, p, p, p]
         L.oracle_metrics.restype = ctypes.c_int
+        L.oracle_portfolio_row.argtypes = [p, u32, u64, u64, p]
+        L.oracle_portfolio_row.restype = None
         _lib = L
     return _lib
 
@@ -157,6 +159,17 @@ def run_analysis(ds, selection: Optional[np.ndarray] = None, n_threads: int = 1,
     if st < -1:
         raise ValueError(f"oracle: ELT record {-st - 2} has an invalid event id")
     return (ylt, mo, inc[:, :n_ev]) if outputs else ylt
+
+
+def portfolio_row(ylt) -> np.ndarray:
+    """Portfolio-scope trial losses: per trial, the sum over layers in layer order, left to
+    right from +0."""
+    y = np.ascontiguousarray(ylt, dtype=np.float64)
+    if y.ndim == 1:
+        y = y[None, :]
+    out = np.empty(y.shape[1])
+    lib().oracle_portfolio_row(_ptr(y), y.shape[0], y.shape[1], y.shape[1], _ptr(out))
+    return out
 
 
 def metrics(ylt_row, p: Sequence[float]):

@@ -83,6 +83,19 @@ int oracle_run_analysis_f32(uint32_t catalogue_size, uint32_t n_elts, const uint
 
 /* ------------------------------------------------------------------------- */
 /* Metrics (reading R11)                                   */
+/* Portfolio-scope trial losses ("portfolio = per-trial sum over layers";
+ * SURVEY 8(f) F1, reading G10): out[t] = ((0 + ylt[0][t]) + ylt[1][t]) + ... + ylt[L-1][t],
+ * left to right in layer order.  ylt is layer-major with row stride ld. */
+void oracle_portfolio_row(const double *ylt, uint32_t n_layers, uint64_t n, uint64_t ld,
+                          double *out)
+{
+    for (uint64_t t = 0; t < n; ++t) {
+        double s = 0.0;
+        for (uint32_t l = 0; l < n_layers; ++l) s = s + ylt[(size_t)l * ld + t];
+        out[t] = s;
+    }
+}
+
 /* ------------------------------------------------------------------------- */
 
 static int o_cmp(const void *a, const void *b)

@@ -474,3 +474,25 @@ def test_f32_within_rounding_bound_of_f64():
     bound = 8 * (10 + 2 + 2) * u32 * (aggR + aggL + float(np.max(ds.rec_losses)) * 2 * 10)
     assert np.all(np.abs(y32 - y64) <= bound)
     assert np.mean(np.abs(y32 - y64) <= 1e-4 * np.abs(y64) + 1e-300) > 0.5
+
+
+# --------------------------------------------------------------------------- portfolio scope
+def test_portfolio_row_pins():
+    """Portfolio-scope losses (per-trial sum over layers): one layer gives the
+    layer's row unchanged; small dyadic YLTs sum exactly (checked in exact rationals); the sum
+    runs left to right in layer order (1e16 + 1 + 1 rounds to 1e16, 1 + 1 + 1e16 does not)."""
+    from fractions import Fraction
+    rng = np.random.default_rng(11)
+    row = rng.lognormal(10, 2, 257)
+    assert np.array_equal(oracle.portfolio_row(row[None, :]), row)
+    for L in (2, 3, 8):
+        y = rng.integers(0, 1 << 30, size=(L, 100)).astype(float) / 1024.0
+        got = oracle.portfolio_row(y)
+        for t in range(100):
+            assert Fraction(got[t]) == sum(Fraction(v) for v in y[:, t])
+    y = np.array([[1e16, 1.0], [1.0, 1.0], [1.0, 1e16]])
+    got = oracle.portfolio_row(y)
+    assert got[0] == 1e16 and got[1] == 1.0000000000000002e16
+    # monotone: adding a layer never lowers a trial's portfolio loss (all entries >= 0)
+    y = rng.lognormal(5, 3, (4, 50))
+    assert (oracle.portfolio_row(y) >= oracle.portfolio_row(y[:3])).all()
