@@ -265,6 +265,8 @@ def main():
     L = ds.n_layers
     d_ylt_loc = torch.empty((L, n_loc), dtype=torch.float64, device=dev)
     d_ylt_full = torch.empty((L, n_total), dtype=torch.float64, device=dev)
+    d_port_full = torch.empty(n_total, dtype=torch.float64, device=dev)  # L > 1 only
+    d_port_loc = torch.empty(n_loc if n_loc else 1, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
     ctx = ara.Context(local, stream)
     ctx.ara_set_precision(args.precision)
@@ -294,9 +296,16 @@ def main():
             b.record(stream)
             scan_ev.append((a, b))
         if world > 1 and args.metrics == "sharded":
-            return [adist.sharded_metrics(ctx, d_ylt_loc[l], n_total, P) for l in range(L)]
+            res = [adist.sharded_metrics(ctx, d_ylt_loc[l], n_total, P) for l in range(L)]
+            if L > 1:  # portfolio scope: per-trial sum over layers
+                ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
+                res.append(adist.sharded_metrics(ctx, d_port_loc, n_total, P))
+            return res
         full = gather()
         res = [ctx.ara_metrics(full[l], P) for l in range(L)]  # A9 (synchronous)
+        if L > 1:  # portfolio scope: per-trial sum over layers
+            ctx.ara_portfolio_ylt(full, d_port_full)
+            res.append(ctx.ara_metrics(d_port_full, P))
         return res
 
     for _ in range(args.warmup):
@@ -400,10 +409,16 @@ def main():
             if world > 1 and args.metrics == "sharded":
                 for l in range(L):
                     adist.sharded_metrics(ctx, d_ylt_loc[l], n_total, P)
+                if L > 1:
+                    ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
+                    adist.sharded_metrics(ctx, d_port_loc, n_total, P)
             else:
                 full = gather()
                 for l in range(L):
                     ctx.ara_metrics(full[l], P)
+                if L > 1:
+                    ctx.ara_portfolio_ylt(full, d_port_full)
+                    ctx.ara_metrics(d_port_full, P)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - tt)
         t_e2e = statistics.median(ts)
@@ -462,6 +477,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "pml": res[0][0].tolist(), "tvar": res[0][1].tolist(),
+            "pml_portfolio": res[L][0].tolist() if L > 1 else None,
+            "tvar_portfolio": res[L][1].tolist() if L > 1 else None,
         }
         s = json.dumps(line)
         print(s, flush=True)

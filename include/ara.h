@@ -238,6 +238,19 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
                        const double *p, double *pml_out, double *tvar_out);
 
 /*
+ * ara_portfolio_ylt -- portfolio-scope trial losses (a loss distribution's
+ * scope is a single layer or the portfolio = per-trial sum over layers):
+ *   d_out[t] = ((0 + YLT[0][t]) + YLT[1][t]) + ... + YLT[L-1][t], left to right in layer order,
+ * for the context's L layers.  Feed d_out to ara_metrics for portfolio PML / TVaR.
+ *   d_ylt    device fp64, YLT[l][t] at d_ylt[l * ylt_ld + t] (as written by ara_run)
+ *   ylt_ld   row stride in elements (0 means n_trials);  d_out  device fp64[n_trials]
+ *   flags    ARA_RUN_SYNC or 0 (stream-ordered)
+ * Errors: ARA_ERR_STATE, ARA_ERR_ARG, ARA_ERR_CUDA.
+ */
+ara_status ara_portfolio_ylt(ara_ctx *ctx, const double *d_ylt, uint64_t n_trials,
+                             uint64_t ylt_ld, double *d_out, uint32_t flags);
+
+/*
  * ara_metrics_sharded -- PML / TVaR of a YLT row that is split over several processes (one
  * contiguous slice per rank, e.g. the trial shards of SURVEY.md 8(e)), without gathering the
  * row: the same MSB radix select as ara_metrics runs pass by pass on every rank's slice, and

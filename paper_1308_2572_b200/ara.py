@@ -31,7 +31,8 @@ ARA_MAX_P = 32
 EXPORTS = ["ara_status_string", "ara_create", "ara_set_precision", "ara_set_stream", "ara_destroy", "ara_last_error",
            "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
            "ara_synchronize",
-           "ara_metrics", "ara_metrics_host", "ara_metrics_sharded", "ara_get_info",
+           "ara_metrics", "ara_metrics_host", "ara_metrics_sharded", "ara_portfolio_ylt",
+           "ara_get_info",
            "ara_layer_store_shape",
            "ara_export_store"]
 
@@ -103,6 +104,7 @@ def _load() -> ctypes.CDLL:
         "ara_synchronize": ([p], i32),
         "ara_metrics": ([p, p, u64, u32, p, p, p], i32),
         "ara_metrics_host": ([p, p, u64, u32, p, p, p], i32),
+        "ara_portfolio_ylt": ([p, p, u64, u64, p, u32], i32),
         "ara_metrics_sharded": ([p, p, u64, u64, u32, p, p, p, p, u64, SHARD_REDUCE, p], i32),
         "ara_get_info": ([p, ctypes.POINTER(Info)], i32),
         "ara_layer_store_shape": ([p, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
@@ -245,6 +247,13 @@ class Context:
                                       d_ylt_row.numel(), pp.shape[0], _hptr(pp), _hptr(pml),
                                       _hptr(tvar)))
         return pml, tvar
+
+    def ara_portfolio_ylt(self, d_ylt, d_out, ylt_ld: int = 0, flags: int = 0):
+        """Per-trial sum over the context's layers (layer order) of a device YLT."""
+        n = d_out.numel()
+        self._check(lib().ara_portfolio_ylt(self._ptr, _dptr(d_ylt, "torch.float64"), n, ylt_ld,
+                                            _dptr(d_out, "torch.float64"), flags))
+        return d_out
 
     def ara_metrics_sharded(self, d_ylt_slice, n_global: int, p: Sequence[float], allreduce):
         """PML / TVaR of a YLT row split over ranks (this rank's slice on the device).

@@ -965,6 +965,24 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
     });
 }
 
+ara_status ara_portfolio_ylt(ara_ctx *ctx, const double *d_ylt, uint64_t n_trials,
+                             uint64_t ylt_ld, double *d_out, uint32_t flags)
+{
+    return guarded(ctx, [&]() -> ara_status {
+        if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
+        if (flags & ~ARA_RUN_SYNC) return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
+        if (n_trials == 0) return ARA_OK;
+        if (!d_ylt || !d_out) return fail(ctx, ARA_ERR_ARG, "device pointer is NULL");
+        const uint64_t ld = ylt_ld ? ylt_ld : n_trials;
+        if (ld < n_trials) return fail(ctx, ARA_ERR_ARG, "ylt_ld < n_trials");
+        cudaError_t e = ara::launch_portfolio_row(d_ylt, ctx->store.n_layers, n_trials, ld, d_out,
+                                                  ctx->sm_count, ctx->stream, &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "portfolio row kernel");
+        if (flags & ARA_RUN_SYNC) ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return ARA_OK;
+    });
+}
+
 ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t n_local,
                                uint64_t n_global, uint32_t n_p, const double *p, double *pml_out,
                                double *tvar_out, void *d_xbuf, uint64_t xbuf_bytes,

@@ -220,6 +220,9 @@ struct MetricsScratch {
     void *d_shard = nullptr;  // sharded metrics: state + per-block tail partials
     size_t shard_bytes = 0;
 };
+cudaError_t launch_portfolio_row(const double *d_ylt, uint32_t n_layers, uint64_t n, uint64_t ld,
+                                 double *d_out, int sm_count, cudaStream_t stream,
+                                 uint64_t *launches);
 // Caller-supplied reduction for the sharded metrics: element-wise SUM across all ranks, in
 // place, of `count` values (int64 if !is_f64, else fp64) at byte offset `offset` of the caller's
 // device exchange buffer, ordered on the context's stream.  Returns 0 on success.

@@ -399,6 +399,19 @@ __global__ void shard_tail_combine_kernel(uint32_t n_p, int blocks, const ShardS
     }
 }
 
+// Portfolio-scope trial losses: out[t] = ((0 + ylt[0][t]) +
+// ylt[1][t]) + ... in layer order -- coalesced reads of the L layer rows, one write.
+__global__ void portfolio_row_kernel(const double *__restrict__ ylt, uint32_t n_layers,
+                                     uint64_t n, uint64_t ld, double *__restrict__ out)
+{
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (uint32_t l = 0; l < n_layers; ++l) s = __dadd_rn(s, ylt[(size_t)l * ld + t]);
+        out[t] = s;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
@@ -536,6 +549,18 @@ cudaError_t launch_metrics_sharded(const double *d_slice, uint64_t n_local, uint
         tvar_out[i] = q + hs[i] / (double)hc[i];
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_portfolio_row(const double *d_ylt, uint32_t n_layers, uint64_t n, uint64_t ld,
+                                 double *d_out, int sm_count, cudaStream_t stream,
+                                 uint64_t *launches)
+{
+    if (n == 0) return cudaSuccess;
+    ++*launches;
+    const uint64_t want = (n + 255) / 256;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)sm_count * 8);
+    portfolio_row_kernel<<<blocks, 256, 0, stream>>>(d_ylt, n_layers, n, ld, d_out);
+    return cudaGetLastError();
 }
 
 }  // namespace ara

@@ -848,3 +848,27 @@ def test_sharded_metrics(stream, R, n):
     for pml, tvar in _threaded_sharded_metrics(slices, n, P_RP):
         assert np.array_equal(pml, opml), (pml, opml)
         np.testing.assert_allclose(tvar, otvar, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("preset,kw", [("portfolio", dict(n_trials=3000, k_min=0, k_max=200)),
+                                       ("tiny", dict(n_trials=500))])
+def test_portfolio_scope_row_and_metrics(stream, preset, kw):
+    """ara_portfolio_ylt: per-trial sum over layers in layer order, bit-identical to the oracle's
+    portfolio row of the oracle's YLT (one layer: the row itself), with a leading dimension;
+    PML / TVaR of it equal the oracle's (PML exact, TVaR 1e-9)."""
+    ds = datagen.generate(datagen.PRESETS[preset].replace(**kw))
+    want_ylt = oracle.run_analysis(ds, n_threads=8)
+    want = oracle.portfolio_row(want_ylt)
+    ctx = make_ctx(ds, stream)
+    n, ld = ds.n_trials, ds.n_trials + 37
+    ylt = torch.zeros((ds.n_layers, ld), dtype=torch.float64, device=DEV)
+    ctx.ara_run(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, ylt_ld=ld,
+                flags=ara.ARA_RUN_SYNC)
+    row = torch.full((n,), float("nan"), dtype=torch.float64, device=DEV)
+    ctx.ara_portfolio_ylt(ylt, row, ylt_ld=ld, flags=ara.ARA_RUN_SYNC)
+    assert_bit_identical(row.cpu().numpy()[None, :], want[None, :])
+    pml, tvar = ctx.ara_metrics(row, P_RP)
+    opml, otvar = oracle.metrics(want, P_RP)
+    assert np.array_equal(pml, opml)
+    np.testing.assert_allclose(tvar, otvar, rtol=1e-9, atol=0)
+    ctx.close()
