@@ -29,6 +29,15 @@
 #include "ara_internal.h"
 #include "scan_common.cuh"
 
+// ARA_ABLATION (tuning builds only, tools/tune_scan.py with ARA_LIB_VARIANT): time the scan with
+// phases removed, for a Fig. graph11-style breakdown:
+// 1 = ids + row index + ELT sum of placeholders (no row gather), 2 = + row gather, 3 = +
+// financial terms, unset = + occurrence / aggregate terms (the real kernel).  The YLT of an
+// ablation build is meaningless.
+#ifndef ARA_ABLATION
+#define ARA_ABLATION 0
+#endif
+
 namespace ara {
 namespace {
 
@@ -52,8 +61,12 @@ __device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
             const int j = PER * i + q;
+#if ARA_ABLATION == 1 || ARA_ABLATION == 2  // phase ablation (timing only): no financial terms
+            f[j] = r[i].v[q];
+#else
             const R l = rsub(rmul(r[i].v[q], rate[j]), ret[j]);
             f[j] = dmin(dmax0(l), lim[j]);
+#endif
         }
     // lines 11-13: lo = ((0 + F_0) + F_1) + ... through the group in column order
     R part = R(0);
@@ -68,6 +81,13 @@ __device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
         part = x;  // valid in lane h after hop h
     }
     // A5-A7 (valid in lane G-1)
+#if ARA_ABLATION >= 1 && ARA_ABLATION <= 3  // phase ablation: no occurrence / aggregate terms
+    S = radd(S, part);
+    lr = S;
+    oc_out = part;
+    inc_out = part;
+    return;
+#endif
     const R oc = dmin(dmax0(rsub(part, occ_ret)), occ_lim);  // line 16
     S = radd(S, oc);                                          // line 19
     const R Cd = dmin(dmax0(rsub(S, agg_ret)), agg_lim);      // line 22
@@ -95,8 +115,16 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
                                        uint32_t idx, Chunk<R> (&r)[CH])
 {
     const R *p = my_rows + (size_t)idx * stride;
+#if ARA_ABLATION == 1  // phase ablation (timing only): ids and row indices, no row gather
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+#pragma unroll
+        for (int q = 0; q < Chunk<R>::N; ++q) r[i].v[q] = (R)((idx >> q) & 7u);
+    (void)p;
+#else
 #pragma unroll
     for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
+#endif
 }
 
 template <int G, int CH, bool X, typename R, bool BAL, int MM, int D>
