@@ -17,6 +17,8 @@
 #include <vector>
 
 #include "ara.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "ara_internal.h"
 
 struct ara_ctx {
@@ -134,10 +136,17 @@ void free_layers(ara_ctx *ctx)
     ctx->have_layers = false;
 }
 
+// NVTX range around every C-ABI call (header-only NVTX3; visible in nsys / ncu timelines).
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <typename F>
-ara_status guarded(ara_ctx *ctx, F &&f)
+ara_status guarded(ara_ctx *ctx, const char *name, F &&f)
 {
     if (!ctx) return ARA_ERR_ARG;
+    NvtxRange range(name);
     try {
         ctx->err.clear();
         DeviceGuard g(ctx->device);
@@ -574,7 +583,7 @@ ara_status ara_create(int cuda_device, void *cuda_stream, ara_ctx **out)
 
 ara_status ara_set_precision(ara_ctx *ctx, uint32_t bits)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (bits != 32 && bits != 64)
             return fail(ctx, ARA_ERR_ARG, "precision %u bits: 32 or 64 expected", bits);
         if ((int)bits != ctx->bits) {
@@ -588,7 +597,7 @@ ara_status ara_set_precision(ara_ctx *ctx, uint32_t bits)
 
 ara_status ara_set_stream(ara_ctx *ctx, void *cuda_stream)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         ctx->stream = (cudaStream_t)cuda_stream;
         return ARA_OK;
@@ -628,7 +637,7 @@ ara_status ara_load_elts(ara_ctx *ctx, uint32_t catalogue_size, uint32_t n_elts,
                          const uint64_t *rec_offsets, const uint32_t *rec_event_ids,
                          const double *rec_losses, const ara_fin_terms *fin)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (catalogue_size == 0 || catalogue_size == UINT32_MAX)
             return fail(ctx, ARA_ERR_ARG, "catalogue_size %u outside [1, 2^32-2]", catalogue_size);
         if (n_elts == 0) return fail(ctx, ARA_ERR_ARG, "n_elts is 0");
@@ -687,7 +696,7 @@ ara_status ara_load_elts(ara_ctx *ctx, uint32_t catalogue_size, uint32_t n_elts,
 ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms *terms,
                           const uint32_t *elt_offsets, const uint32_t *elt_index)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (!ctx->have_elts) return fail(ctx, ARA_ERR_STATE, "ara_load_elts has not succeeded");
         if (n_layers == 0) return fail(ctx, ARA_ERR_ARG, "n_layers is 0");
         if (!terms || !elt_offsets || !elt_index)
@@ -793,7 +802,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
 ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
                            const uint32_t *d_event_ids, const ara_outputs *out, uint32_t flags)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
         if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE | ARA_RUN_HOIST))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
@@ -851,7 +860,7 @@ ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offs
 
 ara_status ara_synchronize(ara_ctx *ctx)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         ARA_CUDA(ctx, cudaGetLastError());
         return check_device_error(ctx);
     });
@@ -861,7 +870,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
                         const uint32_t *h_event_ids, double *h_ylt, uint64_t ylt_ld,
                         uint32_t flags)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
         if (flags & ~(ARA_RUN_SYNC | ARA_RUN_VALIDATE | ARA_RUN_BALANCE | ARA_RUN_HOIST))
             return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
@@ -952,7 +961,7 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
 ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32_t n_p,
                        const double *p, double *pml_out, double *tvar_out)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
         ara_status s = validate_p(ctx, n_p, p);
         if (s != ARA_OK) return s;
@@ -968,7 +977,7 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
 ara_status ara_portfolio_ylt(ara_ctx *ctx, const double *d_ylt, uint64_t n_trials,
                              uint64_t ylt_ld, double *d_out, uint32_t flags)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "ara_set_layers has not succeeded");
         if (flags & ~ARA_RUN_SYNC) return fail(ctx, ARA_ERR_ARG, "unknown flags 0x%x", flags);
         if (n_trials == 0) return ARA_OK;
@@ -988,7 +997,7 @@ ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t
                                double *tvar_out, void *d_xbuf, uint64_t xbuf_bytes,
                                ara_shard_reduce reduce, void *user)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (n_global == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
         ara_status s = validate_p(ctx, n_p, p);
         if (s != ARA_OK) return s;
@@ -1011,7 +1020,7 @@ ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t
 ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, uint32_t n_p,
                             const double *p, double *pml_out, double *tvar_out)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
         ara_status s = validate_p(ctx, n_p, p);
         if (s != ARA_OK) return s;
@@ -1063,7 +1072,7 @@ ara_status ara_layer_store_shape(const ara_ctx *ctx, uint32_t layer, uint32_t *n
 
 ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, double *h_rows)
 {
-    return guarded(ctx, [&]() -> ara_status {
+    return guarded(ctx, __func__, [&]() -> ara_status {
         if (!ctx->have_layers) return fail(ctx, ARA_ERR_STATE, "no layers");
         const ara::DeviceStore &st = ctx->store;
         if (layer >= st.n_layers) return fail(ctx, ARA_ERR_ARG, "layer %u out of range", layer);
