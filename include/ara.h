@@ -86,7 +86,9 @@ typedef struct {
                                length on the device and handed out in warp-sized batches, so
                                the thread groups of a warp run trials of nearly equal length.
                                This is the default schedule; the flag is accepted for clarity.
-                               Results are identical under any schedule.                     */
+                               When the previous run on this context found all trials equally
+                               long, the sort is replaced by the identity order.  Results are
+                               identical under any schedule.                                 */
 #define ARA_RUN_HOIST 8u    /* hoisted scan (deferred exact lever): Alg. 1
                                lines 4-17 depend only on (event, layer), so each run first
                                evaluates them once per distinct event of the layers' union
@@ -175,6 +177,10 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
  * Without ARA_RUN_SYNC the call only enqueues work on the context stream and returns ARA_OK;
  * an event id outside [1, C] then reads the zero row (never out of bounds) and sets a device
  * error flag that the next ara_synchronize() (or synchronous call) reports as ARA_ERR_RANGE.
+ * Performance heuristics (never results): in row addressing mode 2 each run samples 65,536 of
+ * the YET's ids (hit probe) and skips the presence-bitmap test when >= 99% are in the store;
+ * the length check / probe counts of a run are copied back asynchronously and steer the next
+ * run's schedule and kernel choice (see ARA_RUN_BALANCE).
  * Errors: ARA_ERR_STATE, ARA_ERR_ARG, ARA_ERR_RANGE, ARA_ERR_VALIDATION, ARA_ERR_CUDA.
  */
 ara_status ara_run(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_trial_offsets,
