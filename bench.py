@@ -127,7 +127,7 @@ class ClockSampler:
                 "samples": len(rows), "reasons": reasons}
 
 
-def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0):
+def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0, per_core: bool = True):
     """The oracle as it stands, on this host's cores, on a bounded sample of the workload.
 
     The sample grows until one run takes about ``target_s``.  The oracle builds its direct access
@@ -158,11 +158,13 @@ def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0):
     value = n_ev * spec.n_layers / work
     # one thread on a ~2 s slice: the per-core rate (the paper's sequential C++ did
     # 2.96e6 trial-events/s on one i7-2600 core)
-    n1 = max(1, min(spec.n_trials, int(2.0 * value / threads / max(1, k * spec.n_layers))))
-    t1, n_ev1 = run(n1, 1)
-    per_core = n_ev1 * spec.n_layers / max(t1 - t_build, 1e-9)
+    per_core_value = None
+    if per_core:
+        n1 = max(1, min(spec.n_trials, int(2.0 * value / threads / max(1, k * spec.n_layers))))
+        t1, n_ev1 = run(n1, 1)
+        per_core_value = n_ev1 * spec.n_layers / max(t1 - t_build, 1e-9)
     return {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "per_core_value": per_core,
+            "per_core_value": per_core_value,
             "sample": f"first {n_tr} trials x {k} events of the {spec.name} workload "
                       f"({n_ev * spec.n_layers} trial-events, {spec.n_layers} layer(s)); "
                       f"oracle/oracle.c with {threads} threads: {t:.1f} s, minus {t_build:.2f} s "
@@ -175,11 +177,13 @@ def run_reference(args, spec):
     if rank != 0:
         return 0
     ds = datagen.generate(spec, with_yet=False)
-    per_step = max(10.0, 60.0 / max(1, args.steps + args.warmup))
+    # each step a bounded sample: the whole --steps K --warmup W run stays near two minutes
+    per_step = max(2.0, 120.0 / max(1, args.steps + args.warmup))
     cb = None
     vals = []
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline_measure(spec, ds, target_s=min(per_step, 30.0))
+        cb = cpu_baseline_measure(spec, ds, target_s=min(per_step, 30.0),
+                                  per_core=i == args.warmup + args.steps - 1)
         if i >= args.warmup:
             vals.append(cb["value"])
     value = statistics.median(vals)
