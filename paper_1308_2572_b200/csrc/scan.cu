@@ -455,14 +455,19 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     return cudaGetLastError();
 }
 
-// Map mode dispatch; the F4 outputs (X) always use the dense rows through the map.
+// Map mode dispatch.
 template <int G, int CH, int MINB = 1, bool X = false, typename R = double, bool BAL = false,
           int D = 2>
 cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
 {
-    if (!X && st.map_mode == 1)
-        return launch_gcm<G, CH, MINB, X, R, BAL, X ? 0 : 1, D>(st, s, sm_count, stream);
+    // The per-layer direct rows exist only when the union-row store does not serve the layers
+    // (then the F4 outputs, which always use the per-layer kernel, read the dense rows through
+    // the map); the F4 outputs read direct rows without the bitmap (mode 1).
+    if (!st.d_rows_direct)
+        return launch_gcm<G, CH, MINB, X, R, BAL, 0, D>(st, s, sm_count, stream);
+    if (st.map_mode == 1 || (X && st.map_mode == 2))
+        return launch_gcm<G, CH, MINB, X, R, BAL, 1, D>(st, s, sm_count, stream);
     if (!X && st.map_mode == 2)
         return launch_gcm<G, CH, MINB, X, R, BAL, X ? 0 : 2, D>(st, s, sm_count, stream);
     return launch_gcm<G, CH, MINB, X, R, BAL, 0, D>(st, s, sm_count, stream);
@@ -577,7 +582,7 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
         switch (st.width) {
             case 4: return launch_gc<1, 1, 1, true>(st, s, sm_count, stream);
             case 8: return launch_gc<2, 1, 1, true>(st, s, sm_count, stream);
-            case 16: return launch_gc<2, 2, 1, true>(st, s, sm_count, stream);
+            case 16: return launch_gc<2, 2, 3, true>(st, s, sm_count, stream);
             case 32: return launch_gc<4, 2, 1, true>(st, s, sm_count, stream);
             case 48: return launch_gc<4, 3, 1, true>(st, s, sm_count, stream);
             case 64: return launch_gc<4, 4, 1, true>(st, s, sm_count, stream);
