@@ -267,10 +267,12 @@ def main():
     d_off = h_off.to(dev).view(torch.uint64)
     d_ids = h_ids.to(dev).view(torch.uint32)
     L = ds.n_layers
-    d_ylt_loc = torch.empty((L, n_loc), dtype=torch.float64, device=dev)
-    d_ylt_full = torch.empty((L, n_total), dtype=torch.float64, device=dev)
-    d_port_full = torch.empty(n_total, dtype=torch.float64, device=dev)  # L > 1 only
-    d_port_loc = torch.empty(n_loc if n_loc else 1, dtype=torch.float64, device=dev)
+    # YLT rows 0..L-1 and, for L > 1, the portfolio-scope row L
+    L1 = L + 1 if L > 1 else L
+    d_ylt_buf = torch.empty((L1, n_loc), dtype=torch.float64, device=dev)
+    d_ylt_loc = d_ylt_buf[:L]
+    d_full_buf = torch.empty((L1, n_total), dtype=torch.float64, device=dev)
+    d_port_loc = d_ylt_buf[L] if L > 1 else None
     stream = torch.cuda.current_stream(dev)
     ctx = ara.Context(local, stream)
     ctx.ara_set_precision(args.precision)
@@ -285,8 +287,16 @@ def main():
 
     def gather():
         if world == 1:
-            return d_ylt_loc
-        return adist.gather_ylt(d_ylt_loc, n_total, out=d_ylt_full)
+            return d_ylt_buf
+        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L])
+        return d_full_buf
+
+    def post_metrics(rows):
+        """A9 on the gathered YLT rows (+ the portfolio row): one batched call (synchronous)."""
+        if L > 1:
+            ctx.ara_portfolio_ylt(rows[:L], rows[L])
+        pml, tvar = ctx.ara_metrics_rows(rows[:L1], P)
+        return [(pml[i], tvar[i]) for i in range(L1)]
 
     scan_ev = []
     run_flags = ara.ARA_RUN_HOIST if args.hoist else 0
@@ -305,12 +315,7 @@ def main():
                 ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
                 res.append(adist.sharded_metrics(ctx, d_port_loc, n_total, P))
             return res
-        full = gather()
-        res = [ctx.ara_metrics(full[l], P) for l in range(L)]  # A9 (synchronous)
-        if L > 1:  # portfolio scope: per-trial sum over layers
-            ctx.ara_portfolio_ylt(full, d_port_full)
-            res.append(ctx.ara_metrics(d_port_full, P))
-        return res
+        return post_metrics(gather())  # A9 (+ portfolio scope)
 
     for _ in range(args.warmup):
         step(False)
@@ -417,12 +422,7 @@ def main():
                     ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
                     adist.sharded_metrics(ctx, d_port_loc, n_total, P)
             else:
-                full = gather()
-                for l in range(L):
-                    ctx.ara_metrics(full[l], P)
-                if L > 1:
-                    ctx.ara_portfolio_ylt(full, d_port_full)
-                    ctx.ara_metrics(d_port_full, P)
+                post_metrics(gather())
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - tt)
         t_e2e = statistics.median(ts)

@@ -244,6 +244,17 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
                        const double *p, double *pml_out, double *tvar_out);
 
 /*
+ * ara_metrics_rows -- ara_metrics for n_rows rows of one matrix in the same radix-select passes
+ * (e.g. every layer of a YLT plus the portfolio row): one cooperative launch per
+ * floor(64 / n_p) rows instead of one per row.  Row r is d_rows[r * ld .. r * ld + n) (ld = 0
+ * means n).  pml_out / tvar_out are host arrays [n_rows][n_p].  Results equal ara_metrics on
+ * each row.  Synchronous.  Errors: as ara_metrics.
+ */
+ara_status ara_metrics_rows(ara_ctx *ctx, const double *d_rows, uint32_t n_rows, uint64_t ld,
+                            uint64_t n, uint32_t n_p, const double *p, double *pml_out,
+                            double *tvar_out);
+
+/*
  * ara_portfolio_ylt -- portfolio-scope trial losses (a loss distribution's
  * scope is a single layer or the portfolio = per-trial sum over layers):
  *   d_out[t] = ((0 + YLT[0][t]) + YLT[1][t]) + ... + YLT[L-1][t], left to right in layer order,

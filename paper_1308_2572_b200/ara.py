@@ -31,7 +31,8 @@ ARA_MAX_P = 32
 EXPORTS = ["ara_status_string", "ara_create", "ara_set_precision", "ara_set_stream", "ara_destroy", "ara_last_error",
            "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
            "ara_synchronize",
-           "ara_metrics", "ara_metrics_host", "ara_metrics_sharded", "ara_portfolio_ylt",
+           "ara_metrics", "ara_metrics_host", "ara_metrics_rows", "ara_metrics_sharded",
+           "ara_portfolio_ylt",
            "ara_get_info",
            "ara_layer_store_shape",
            "ara_export_store"]
@@ -105,6 +106,7 @@ def _load() -> ctypes.CDLL:
         "ara_metrics": ([p, p, u64, u32, p, p, p], i32),
         "ara_metrics_host": ([p, p, u64, u32, p, p, p], i32),
         "ara_portfolio_ylt": ([p, p, u64, u64, p, u32], i32),
+        "ara_metrics_rows": ([p, p, u32, u64, u64, u32, p, p, p], i32),
         "ara_metrics_sharded": ([p, p, u64, u64, u32, p, p, p, p, u64, SHARD_REDUCE, p], i32),
         "ara_get_info": ([p, ctypes.POINTER(Info)], i32),
         "ara_layer_store_shape": ([p, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
@@ -246,6 +248,19 @@ class Context:
         self._check(lib().ara_metrics(self._ptr, _dptr(d_ylt_row, "torch.float64"),
                                       d_ylt_row.numel(), pp.shape[0], _hptr(pp), _hptr(pml),
                                       _hptr(tvar)))
+        return pml, tvar
+
+    def ara_metrics_rows(self, d_rows, p: Sequence[float], n: int = 0, ld: int = 0):
+        """PML / TVaR ([rows][n_p] arrays) of every row of a 2-D device tensor in shared passes
+        (``n``: entries per row, default the row length; ``ld``: row stride, default the
+        tensor's)."""
+        pp = np.ascontiguousarray(p, dtype=np.float64)
+        R = d_rows.shape[0]
+        n = n or d_rows.shape[1]
+        ld = ld or d_rows.stride(0)
+        pml = np.empty((R, pp.shape[0])); tvar = np.empty((R, pp.shape[0]))
+        self._check(lib().ara_metrics_rows(self._ptr, _dptr(d_rows, "torch.float64"), R, ld, n,
+                                           pp.shape[0], _hptr(pp), _hptr(pml), _hptr(tvar)))
         return pml, tvar
 
     def ara_portfolio_ylt(self, d_ylt, d_out, ylt_ld: int = 0, flags: int = 0):

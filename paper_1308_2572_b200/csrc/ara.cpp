@@ -966,8 +966,28 @@ ara_status ara_metrics(ara_ctx *ctx, const double *d_ylt_row, uint64_t n, uint32
         ara_status s = validate_p(ctx, n_p, p);
         if (s != ARA_OK) return s;
         if (!d_ylt_row || !pml_out || !tvar_out) return fail(ctx, ARA_ERR_ARG, "NULL pointer");
-        cudaError_t e = ara::launch_metrics(d_ylt_row, n, n_p, p, pml_out, tvar_out, ctx->metrics,
-                                            ctx->sm_count, ctx->device, ctx->stream,
+        cudaError_t e = ara::launch_metrics(d_ylt_row, n, 1, n, n_p, p, pml_out, tvar_out,
+                                            ctx->metrics, ctx->sm_count, ctx->device, ctx->stream,
+                                            &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");
+        return ARA_OK;
+    });
+}
+
+ara_status ara_metrics_rows(ara_ctx *ctx, const double *d_rows, uint32_t n_rows, uint64_t ld,
+                            uint64_t n, uint32_t n_p, const double *p, double *pml_out,
+                            double *tvar_out)
+{
+    return guarded(ctx, __func__, [&]() -> ara_status {
+        if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "metrics over zero trials");
+        ara_status s = validate_p(ctx, n_p, p);
+        if (s != ARA_OK) return s;
+        if (n_rows == 0) return ARA_OK;
+        if (!d_rows || !pml_out || !tvar_out) return fail(ctx, ARA_ERR_ARG, "NULL pointer");
+        const uint64_t stride = ld ? ld : n;
+        if (stride < n) return fail(ctx, ARA_ERR_ARG, "ld < n");
+        cudaError_t e = ara::launch_metrics(d_rows, stride, n_rows, n, n_p, p, pml_out, tvar_out,
+                                            ctx->metrics, ctx->sm_count, ctx->device, ctx->stream,
                                             &ctx->launches);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");
         return ARA_OK;
@@ -1034,7 +1054,7 @@ ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, u
         }
         ARA_CUDA(ctx, cudaMemcpyAsync(ctx->d_row_stage, h_ylt_row, n * 8, cudaMemcpyHostToDevice,
                                       ctx->stream));
-        cudaError_t e = ara::launch_metrics(ctx->d_row_stage, n, n_p, p, pml_out, tvar_out,
+        cudaError_t e = ara::launch_metrics(ctx->d_row_stage, n, 1, n, n_p, p, pml_out, tvar_out,
                                             ctx->metrics, ctx->sm_count, ctx->device,
                                             ctx->stream, &ctx->launches);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "metrics kernel");

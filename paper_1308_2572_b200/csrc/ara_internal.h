@@ -232,9 +232,12 @@ cudaError_t launch_metrics_sharded(const double *d_slice, uint64_t n_local, uint
                                    double *tvar_out, char *d_xbuf, ShardReduce reduce,
                                    void *user, MetricsScratch &scratch, int sm_count,
                                    cudaStream_t stream, uint64_t *launches);
-cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
-                           double *pml_out, double *tvar_out, MetricsScratch &scratch,
-                           int sm_count, int device, cudaStream_t stream, uint64_t *launches);
+// PML/TVaR of n_rows rows (row r at d_rows + r * ld, n entries each) in shared passes;
+// pml_out / tvar_out are [n_rows][n_p].
+cudaError_t launch_metrics(const double *d_rows, uint64_t ld, uint32_t n_rows, uint64_t n,
+                           uint32_t n_p, const double *p, double *pml_out, double *tvar_out,
+                           MetricsScratch &scratch, int sm_count, int device, cudaStream_t stream,
+                           uint64_t *launches);
 
 constexpr uint32_t kErrRange = 1u;
 constexpr uint32_t kErrOffsets = 2u;

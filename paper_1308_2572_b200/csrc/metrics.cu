@@ -27,15 +27,21 @@ constexpr int kThreads = 256;
 constexpr int kBins = 256;
 constexpr int kPasses = 8;
 
+// A batch of R rows (row r at v + r * ld, n entries each) is processed in the same passes: slot
+// s = r * n_p + i is (row r, probability i); R * n_p <= kMaxSlots.  One row is ara_metrics.
+constexpr int kMaxSlots = 64;
+
 struct MetricsParams {
     const double *v;
-    uint64_t n;
+    uint64_t ld;                   // row stride (elements)
+    uint64_t n;                    // entries per row
+    uint32_t n_rows;
     uint32_t n_p;
-    uint64_t rank[ARA_MAX_P];      // 0-based target ranks ceil(p n) - 1
-    uint32_t *hist;                // [kPasses][ARA_MAX_P][kBins]
-    double *part_sum;              // [grid][ARA_MAX_P]
-    unsigned long long *part_cnt;  // [grid][ARA_MAX_P]
-    double *out;                   // [2][n_p]: pml, tvar
+    uint64_t rank[ARA_MAX_P];      // 0-based target ranks ceil(p n) - 1 (same for every row)
+    uint32_t *hist;                // [kPasses][kMaxSlots][kBins]
+    double *part_sum;              // [grid][kMaxSlots]
+    unsigned long long *part_cnt;  // [grid][kMaxSlots]
+    double *out;                   // [2][n_rows * n_p]: pml, tvar
 };
 
 // Order-preserving map of finite doubles to u64 (-0 canonicalised to +0).
@@ -52,171 +58,184 @@ __device__ __forceinline__ double from_key(uint64_t k)
     return __longlong_as_double((long long)b);
 }
 
+// Distinct (row, key prefix under mask) pairs of the slots, row-major, so that the pairs of row r
+// are u in [ubeg[r], ubeg[r + 1]).  Two distinct prefixes of one row are disjoint, so every
+// element adds to at most one histogram.
+__device__ __forceinline__ uint32_t dedup_rows(const uint64_t *prefix, uint32_t n_rows,
+                                               uint32_t n_p, uint64_t mask, uint64_t *uprefix,
+                                               uint32_t *uof, uint32_t *ubeg)
+{
+    uint32_t nu = 0;
+    for (uint32_t r = 0; r < n_rows; ++r) {
+        ubeg[r] = nu;
+        for (uint32_t i = 0; i < n_p; ++i) {
+            const uint32_t sl = r * n_p + i;
+            uint32_t u = ubeg[r];
+            while (u < nu && uprefix[u] != (prefix[sl] & mask)) ++u;
+            if (u == nu) uprefix[nu++] = prefix[sl] & mask;
+            uof[sl] = u;
+        }
+    }
+    ubeg[n_rows] = nu;
+    return nu;
+}
+
 __global__ void __launch_bounds__(kThreads) metrics_kernel(const __grid_constant__ MetricsParams P)
 {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t sh[ARA_MAX_P][kBins];
-    __shared__ uint64_t s_prefix[ARA_MAX_P];  // per probability: key prefix found so far
-    __shared__ uint64_t s_rank[ARA_MAX_P];    // per probability: rank within that prefix
-    __shared__ uint64_t s_uprefix[ARA_MAX_P]; // distinct prefixes of this pass
-    __shared__ uint32_t s_uof[ARA_MAX_P];     // probability -> its distinct prefix
+    extern __shared__ uint32_t sh[];          // [distinct pairs][kBins]
+    __shared__ uint64_t s_prefix[kMaxSlots];  // per slot: key prefix found so far
+    __shared__ uint64_t s_rank[kMaxSlots];    // per slot: rank within that prefix
+    __shared__ uint64_t s_uprefix[kMaxSlots]; // distinct (row, prefix) pairs of this pass
+    __shared__ uint32_t s_uof[kMaxSlots];     // slot -> its distinct pair
+    __shared__ uint32_t s_ubeg[kMaxSlots + 1];
     __shared__ uint32_t s_nu;
-    __shared__ uint64_t s_wsum[kThreads / 32];
-    __shared__ uint64_t s_prefix_n[ARA_MAX_P];
-    __shared__ uint64_t s_rank_n[ARA_MAX_P];
-    __shared__ double s_red[kThreads / 32];
-    __shared__ unsigned long long s_redc[kThreads / 32];
+    __shared__ uint64_t s_prefix_n[kMaxSlots];
+    __shared__ uint64_t s_rank_n[kMaxSlots];
 
-    const uint32_t n_p = P.n_p;
+    const uint32_t n_p = P.n_p, R = P.n_rows, S = R * n_p;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
 
-    for (uint64_t i = gtid; i < (uint64_t)kPasses * ARA_MAX_P * kBins; i += gstride) P.hist[i] = 0;
-    if (threadIdx.x < n_p) {
+    for (uint64_t i = gtid; i < (uint64_t)kPasses * kMaxSlots * kBins; i += gstride)
+        P.hist[i] = 0;
+    if (threadIdx.x < S) {
         s_prefix[threadIdx.x] = 0;
-        s_rank[threadIdx.x] = P.rank[threadIdx.x];
+        s_rank[threadIdx.x] = P.rank[threadIdx.x % n_p];
     }
     grid.sync();
 
     for (int pass = 0; pass < kPasses; ++pass) {
         const int shift = 56 - 8 * pass;
         const uint64_t mask = pass == 0 ? 0ull : (~0ull << (shift + 8));
-        // Probabilities whose prefixes agree share one histogram (early passes: all of them),
-        // and two distinct prefixes of the same length are disjoint, so every element adds to
-        // at most one histogram.
-        if (threadIdx.x == 0) {
-            uint32_t nu = 0;
-            for (uint32_t i = 0; i < n_p; ++i) {
-                uint32_t u = 0;
-                while (u < nu && s_uprefix[u] != (s_prefix[i] & mask)) ++u;
-                if (u == nu) s_uprefix[nu++] = s_prefix[i] & mask;
-                s_uof[i] = u;
-            }
-            s_nu = nu;
-        }
-        for (uint32_t i = threadIdx.x; i < n_p * kBins; i += blockDim.x) (&sh[0][0])[i] = 0;
+        // Probabilities whose prefixes agree share one histogram (early passes: all of a row's)
+        if (threadIdx.x == 0) s_nu = dedup_rows(s_prefix, R, n_p, mask, s_uprefix, s_uof, s_ubeg);
         __syncthreads();
         const uint32_t nu = s_nu;
-        for (uint64_t e0 = gtid - lane; e0 < P.n; e0 += gstride) {  // warp-uniform trip count
-            const uint64_t e = e0 + lane;
-            uint32_t slot = 0xffffffffu;  // (distinct prefix, digit) or none
-            if (e < P.n) {
-                const uint64_t key = to_key(P.v[e]);
-                for (uint32_t u = 0; u < nu; ++u)
-                    if ((key & mask) == s_uprefix[u]) slot = u * kBins + ((key >> shift) & 0xff);
-            }
-            // warp-aggregated histogram update: one atomic per distinct slot in the warp (after
-            // the first passes most warps hold no element of any surviving prefix: skip them)
-            if (__any_sync(0xffffffffu, slot != 0xffffffffu)) {
-                const uint32_t peers = __match_any_sync(0xffffffffu, slot);
-                if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-                    atomicAdd(&sh[0][0] + slot, (uint32_t)__popc(peers));
+        for (uint32_t i = threadIdx.x; i < nu * kBins; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+        for (uint32_t r = 0; r < R; ++r) {
+            const double *v = P.v + (size_t)r * P.ld;
+            const uint32_t u0 = s_ubeg[r], u1 = s_ubeg[r + 1];
+            for (uint64_t e0 = gtid - lane; e0 < P.n; e0 += gstride) {  // warp-uniform trips
+                const uint64_t e = e0 + lane;
+                uint32_t slot = 0xffffffffu;  // (distinct pair, digit) or none
+                if (e < P.n) {
+                    const uint64_t key = to_key(v[e]);
+                    for (uint32_t u = u0; u < u1; ++u)
+                        if ((key & mask) == s_uprefix[u]) slot = u * kBins + ((key >> shift) & 0xff);
+                }
+                // warp-aggregated histogram update: one atomic per distinct slot in the warp
+                // (after the first passes most warps hold no element of a surviving prefix)
+                if (__any_sync(0xffffffffu, slot != 0xffffffffu)) {
+                    const uint32_t peers = __match_any_sync(0xffffffffu, slot);
+                    if (slot != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                        atomicAdd(sh + slot, (uint32_t)__popc(peers));
+                }
             }
         }
         __syncthreads();
-        uint32_t *gh = P.hist + (size_t)pass * ARA_MAX_P * kBins;
+        uint32_t *gh = P.hist + (size_t)pass * kMaxSlots * kBins;
         for (uint32_t i = threadIdx.x; i < nu * kBins; i += blockDim.x) {
-            const uint32_t c = (&sh[0][0])[i];
+            const uint32_t c = sh[i];
             if (c) atomicAdd(gh + i, c);
         }
         grid.sync();
-        // Every block reads the merged histograms (one bin per thread), scans them, and each
-        // probability finds the bin holding its rank: no serial walk over dependent L2 loads.
-        static_assert(kThreads == kBins, "one bin per thread");
-        for (uint32_t u = 0; u < nu; ++u) {
-            const uint64_t cnt = __ldcg(gh + (size_t)u * kBins + threadIdx.x);
-            uint64_t incl = cnt;  // inclusive prefix sum over the 256 bins
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
-            }
-            if (lane == 31) s_wsum[threadIdx.x >> 5] = incl;
-            __syncthreads();
-            uint64_t before = 0;
-            for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) before += s_wsum[w];
-            incl += before;
-            const uint64_t excl = incl - cnt;
-            for (uint32_t i = 0; i < n_p; ++i) {
-                const uint64_t r = s_rank[i];
-                if (s_uof[i] == u && r >= excl && r < incl) {
-                    s_prefix_n[i] = s_prefix[i] | ((uint64_t)threadIdx.x << shift);
-                    s_rank_n[i] = r - excl;
+        // Every block reads the merged histograms and each slot finds the bin holding its rank:
+        // one warp per distinct pair (8 bins per lane, a warp-shuffle scan of the lane totals),
+        // no block-wide barriers inside and no serial walk over dependent L2 loads.
+        static_assert(kBins == 32 * 8, "8 bins per lane");
+        {
+            const uint32_t warp = threadIdx.x >> 5;
+            for (uint32_t u = warp; u < nu; u += kThreads / 32) {
+                uint32_t row = 0;
+                while (s_ubeg[row + 1] <= u) ++row;  // pairs are row-major
+                const uint32_t *hu = gh + (size_t)u * kBins + lane * 8;
+                uint64_t c[8], tot = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    c[k] = __ldcg(hu + k);
+                    tot += c[k];
+                }
+                uint64_t incl = tot;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                const uint64_t excl = incl - tot;
+                for (uint32_t i = row * n_p; i < (row + 1) * n_p; ++i) {
+                    const uint64_t r = s_rank[i];
+                    if (s_uof[i] == u && r >= excl && r < incl) {  // exactly one lane
+                        uint64_t acc = excl;
+                        for (int k = 0; k < 8; ++k) {
+                            if (r < acc + c[k]) {
+                                s_prefix_n[i] = s_prefix[i] | ((uint64_t)(lane * 8 + k) << shift);
+                                s_rank_n[i] = r - acc;
+                                break;
+                            }
+                            acc += c[k];
+                        }
+                    }
                 }
             }
-            __syncthreads();
         }
-        if (threadIdx.x < n_p) {
+        __syncthreads();
+        if (threadIdx.x < S) {
             s_prefix[threadIdx.x] = s_prefix_n[threadIdx.x];
             s_rank[threadIdx.x] = s_rank_n[threadIdx.x];
         }
         __syncthreads();
     }
 
-    // Tail sums over this block's contiguous chunk in a fixed order, once per distinct PML (equal
-    // order statistics have equal tails).  The sum is of (v - PML) >= 0, so TVaR = PML +
-    // mean(v - PML) >= PML holds exactly and the rounding error scales with the tail's spread.
-    if (threadIdx.x == 0) {
-        uint32_t nu = 0;
-        for (uint32_t i = 0; i < n_p; ++i) {
-            uint32_t u = 0;
-            while (u < nu && s_uprefix[u] != s_prefix[i]) ++u;
-            if (u == nu) s_uprefix[nu++] = s_prefix[i];
-            s_uof[i] = u;
-        }
-        s_nu = nu;
-    }
+    // Tail sums over this block's contiguous chunk of each row in a fixed order, once per
+    // distinct PML of the row (equal order statistics have equal tails).  The sum is of
+    // (v - PML) >= 0, so TVaR = PML + mean(v - PML) >= PML holds exactly and the rounding error
+    // scales with the tail's spread.
+    if (threadIdx.x == 0) s_nu = dedup_rows(s_prefix, R, n_p, ~0ull, s_uprefix, s_uof, s_ubeg);
     __syncthreads();
-    const uint32_t nu = s_nu;
     const uint64_t chunk = (P.n + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = (uint64_t)blockIdx.x * chunk;
     const uint64_t hi = lo + chunk < P.n ? lo + chunk : P.n;
-    const int warp = threadIdx.x >> 5;
-    for (uint32_t u = 0; u < nu; ++u) {
+    const uint32_t warp = threadIdx.x >> 5, nu_t = s_nu;
+    // one warp per distinct (row, PML) pair: a fixed assignment and a fixed order, so the
+    // partial sums are deterministic; no block-wide barriers
+    for (uint32_t u = warp; u < nu_t; u += kThreads / 32) {
+        uint32_t row = 0;
+        while (s_ubeg[row + 1] <= u) ++row;
+        const double *v = P.v + (size_t)row * P.ld;
         const uint64_t q = s_uprefix[u];
         const double qv = from_key(q);
-        double s = 0.0;
+        double sum = 0.0;
         unsigned long long c = 0;
-        for (uint64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-            const double x = P.v[e];
+        for (uint64_t e = lo + lane; e < hi; e += 32) {
+            const double x = v[e];
             if (to_key(x) >= q) {
-                s += x - qv;
+                sum += x - qv;
                 ++c;
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
-            s += __shfl_down_sync(0xffffffffu, s, o);
+            sum += __shfl_down_sync(0xffffffffu, sum, o);
             c += __shfl_down_sync(0xffffffffu, c, o);
         }
         if (lane == 0) {
-            s_red[warp] = s;
-            s_redc[warp] = c;
+            P.part_sum[(size_t)blockIdx.x * kMaxSlots + u] = sum;
+            P.part_cnt[(size_t)blockIdx.x * kMaxSlots + u] = c;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double bs = 0.0;
-            unsigned long long bc = 0;
-            for (int w = 0; w < kThreads / 32; ++w) {
-                bs += s_red[w];
-                bc += s_redc[w];
-            }
-            P.part_sum[(size_t)blockIdx.x * ARA_MAX_P + u] = bs;
-            P.part_cnt[(size_t)blockIdx.x * ARA_MAX_P + u] = bc;
-        }
-        __syncthreads();
     }
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x < n_p) {
+    if (blockIdx.x == 0 && threadIdx.x < S) {
         const uint32_t i = threadIdx.x, u = s_uof[i];
-        double s = 0.0;
+        double sum = 0.0;
         unsigned long long c = 0;
         for (uint32_t b = 0; b < gridDim.x; ++b) {
-            s += __ldcg(P.part_sum + (size_t)b * ARA_MAX_P + u);
-            c += __ldcg(P.part_cnt + (size_t)b * ARA_MAX_P + u);
+            sum += __ldcg(P.part_sum + (size_t)b * kMaxSlots + u);
+            c += __ldcg(P.part_cnt + (size_t)b * kMaxSlots + u);
         }
         const double q = from_key(s_prefix[i]);
         P.out[i] = q;
-        P.out[n_p + i] = q + s / (double)c;
+        P.out[S + i] = q + sum / (double)c;
     }
 }
 
@@ -414,61 +433,77 @@ __global__ void portfolio_row_kernel(const double *__restrict__ ylt, uint32_t n_
 
 }  // namespace
 
-cudaError_t launch_metrics(const double *d_row, uint64_t n, uint32_t n_p, const double *p,
-                           double *pml_out, double *tvar_out, MetricsScratch &scratch,
-                           int sm_count, int device, cudaStream_t stream, uint64_t *launches)
+cudaError_t launch_metrics(const double *d_rows, uint64_t ld, uint32_t n_rows, uint64_t n,
+                           uint32_t n_p, const double *p, double *pml_out, double *tvar_out,
+                           MetricsScratch &scratch, int sm_count, int device, cudaStream_t stream,
+                           uint64_t *launches)
 {
     cudaError_t e;
+    int per_sm = 4;  // blocks per SM (tuning: ARA_METRICS_BLOCKS_PER_SM; 4 measured best)
+    if (const char *bps = getenv("ARA_METRICS_BLOCKS_PER_SM")) per_sm = atoi(bps);
+    if (per_sm < 1) per_sm = 1;
     if (scratch.d_buf == nullptr) {
-        int occ = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, metrics_kernel, kThreads, 0);
-        if (e != cudaSuccess) return e;
         int coop = 0;
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
-        if (!coop || occ < 1) return cudaErrorNotSupported;
-        int per_sm = 4;  // blocks per SM (tuning: ARA_METRICS_BLOCKS_PER_SM; 4 measured best)
-        if (const char *b = getenv("ARA_METRICS_BLOCKS_PER_SM")) per_sm = atoi(b);
-        if (per_sm < 1) per_sm = 1;
-        scratch.grid = sm_count * (occ < per_sm ? occ : per_sm);
-        scratch.bytes = (size_t)kPasses * ARA_MAX_P * kBins * 4 +
-                        (size_t)scratch.grid * ARA_MAX_P * 16 + 2 * ARA_MAX_P * 8;
+        if (!coop) return cudaErrorNotSupported;
+        e = cudaFuncSetAttribute(metrics_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxSlots * kBins * 4);
+        if (e != cudaSuccess) return e;
+        scratch.grid = sm_count * per_sm;  // upper bound; the launch clamps to co-residency
+        scratch.bytes = (size_t)kPasses * kMaxSlots * kBins * 4 +
+                        (size_t)scratch.grid * kMaxSlots * 16 + 2 * kMaxSlots * 8;
         e = cudaMalloc(&scratch.d_buf, scratch.bytes);
         if (e != cudaSuccess) return e;
     }
-    MetricsParams P{};
-    P.v = d_row;
-    P.n = n;
-    P.n_p = n_p;
+    uint64_t rank[ARA_MAX_P];
     for (uint32_t i = 0; i < n_p; ++i) {
         // nearest rank, computed in fp64 exactly as the reading states: ceil(p * n)
         uint64_t r = (uint64_t)ceil(p[i] * (double)n);
         if (r < 1) r = 1;
         if (r > n) r = n;
-        P.rank[i] = r - 1;
+        rank[i] = r - 1;
     }
-    char *b = (char *)scratch.d_buf;
-    P.hist = (uint32_t *)b;
-    b += (size_t)kPasses * ARA_MAX_P * kBins * 4;
-    P.part_sum = (double *)b;
-    b += (size_t)scratch.grid * ARA_MAX_P * 8;
-    P.part_cnt = (unsigned long long *)b;
-    b += (size_t)scratch.grid * ARA_MAX_P * 8;
-    P.out = (double *)b;
-    int grid = scratch.grid;
-    const uint64_t want = (n + kThreads - 1) / kThreads;
-    if ((uint64_t)grid > want) grid = (int)want;
-    void *args[] = {&P};
-    ++*launches;
-    e = cudaLaunchCooperativeKernel((void *)metrics_kernel, grid, kThreads, args, 0, stream);
-    if (e != cudaSuccess) return e;
-    double host[2 * ARA_MAX_P];
-    e = cudaMemcpyAsync(host, P.out, 2 * n_p * sizeof(double), cudaMemcpyDeviceToHost, stream);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) return e;
-    for (uint32_t i = 0; i < n_p; ++i) {
-        pml_out[i] = host[i];
-        tvar_out[i] = host[n_p + i];
+    const uint32_t rows_per = kMaxSlots / n_p;  // rows per launch (n_p <= ARA_MAX_P <= 64)
+    for (uint32_t r0 = 0; r0 < n_rows; r0 += rows_per) {
+        const uint32_t R = std::min(rows_per, n_rows - r0), S = R * n_p;
+        MetricsParams P{};
+        P.v = d_rows + (size_t)r0 * ld;
+        P.ld = ld;
+        P.n = n;
+        P.n_rows = R;
+        P.n_p = n_p;
+        for (uint32_t i = 0; i < n_p; ++i) P.rank[i] = rank[i];
+        char *b = (char *)scratch.d_buf;
+        P.hist = (uint32_t *)b;
+        b += (size_t)kPasses * kMaxSlots * kBins * 4;
+        P.part_sum = (double *)b;
+        b += (size_t)scratch.grid * kMaxSlots * 8;
+        P.part_cnt = (unsigned long long *)b;
+        b += (size_t)scratch.grid * kMaxSlots * 8;
+        P.out = (double *)b;
+        const size_t smem = (size_t)S * kBins * 4;  // one histogram per distinct pair (<= S)
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, metrics_kernel, kThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorNotSupported;
+        int grid = sm_count * std::min(occ, per_sm);
+        if (grid > scratch.grid) grid = scratch.grid;
+        const uint64_t want = (n + kThreads - 1) / kThreads;
+        if ((uint64_t)grid > want) grid = (int)want;
+        void *args[] = {&P};
+        ++*launches;
+        e = cudaLaunchCooperativeKernel((void *)metrics_kernel, grid, kThreads, args, smem,
+                                        stream);
+        if (e != cudaSuccess) return e;
+        double host[2 * kMaxSlots];
+        e = cudaMemcpyAsync(host, P.out, 2 * S * sizeof(double), cudaMemcpyDeviceToHost, stream);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return e;
+        for (uint32_t i = 0; i < S; ++i) {
+            pml_out[(size_t)r0 * n_p + i] = host[i];
+            tvar_out[(size_t)r0 * n_p + i] = host[S + i];
+        }
     }
     return cudaSuccess;
 }
