@@ -193,6 +193,47 @@ def test_absent_events_only(stream):
     assert_bit_identical(gpu_ylt(ds, stream), want)
 
 
+@pytest.mark.parametrize("C_big", [(1 << 31) + 1000, 0xFFFFFFFE])
+def test_catalogue_at_max_ids(stream, C_big):
+    """Maximum sizes of the id space: catalogues past 2^31 and at the API's maximum C = 2^32 - 2
+    (ara.h ara_load_elts; C = 2^32 - 1 is rejected).  Relabelling every event id by a constant shift is a
+    bijection of the catalogue, so the YLT of the shifted portfolio equals the oracle's YLT of the
+    original one (C = 1000) bit for bit.  The dense catalogue map then has 2^31-2^32 entries and
+    the rows-by-id store does not fit, so this covers the catalogue-map path at its index limits;
+    an id one past C (up to 2^32 - 1) is still rejected."""
+    import dataclasses
+
+    psutil = pytest.importorskip("psutil")
+    need = 3 * (C_big + 1) * 4 + (8 << 30)  # host map + stamp vectors, headroom
+    if psutil.virtual_memory().available < need:
+        pytest.skip(f"needs {need >> 30} GiB of free host memory")
+    ds = datagen.generate(datagen.PRESETS["tiny"].replace(seed=77, n_trials=600))
+    want = oracle.run_analysis(ds)
+    shift = np.uint64(C_big - ds.catalogue_size)
+    big = dataclasses.replace(
+        ds, catalogue_size=C_big,
+        rec_event_ids=(ds.rec_event_ids.astype(np.uint64) + shift).astype(np.uint32),
+        events=(ds.events.astype(np.uint64) + shift).astype(np.uint32))
+    assert int(big.events.max()) <= C_big and int(big.rec_event_ids.min()) > C_big - 1000
+    ctx = make_ctx(big, stream)
+    try:
+        assert_bit_identical(gpu_ylt(big, stream, ctx=ctx), want)
+        assert_bit_identical(gpu_ylt(big, stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
+        bad = big.events.copy()
+        bad[len(bad) // 2] = C_big + 1
+        with pytest.raises(ara.AraError) as ei:
+            gpu_ylt(big, stream, ctx=ctx, events=bad)
+        assert ei.value.status_name == "ARA_ERR_RANGE"
+    finally:
+        ctx.close()
+    if C_big == 0xFFFFFFFE:
+        ctx = ara.Context(0, stream)
+        with pytest.raises(ara.AraError, match="ARA_ERR_ARG"):
+            ctx.ara_load_elts(C_big + 1, big.rec_offsets, big.rec_event_ids, big.rec_losses,
+                              big.fin)
+        ctx.close()
+
+
 # --------------------------------------------------------------------------- row addressing
 @pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("preset,kw", [
