@@ -583,6 +583,31 @@ def test_dynamic_balance_scheduling(stream, preset, k):
     ctx.close()
 
 
+@pytest.mark.parametrize("preset,long_lens", [
+    ("tiny", (3_000_001, (1 << 20) + 3, 2_500_000)),
+    ("portfolio", (1_000_003, 1 << 19, 777_777)),
+])
+def test_extreme_length_skew(stream, preset, long_lens):
+    """Three trials of 0.5M-3M events among 4000 trials of 0-19 events (the length-sorted warp
+    batches, the dynamic tickets and the hoisted scan under extreme skew; the running sum over
+    millions of events): the oracle's YLT bit for bit in every schedule."""
+    import dataclasses
+
+    ds = datagen.generate(datagen.PRESETS[preset].replace(seed=31, n_trials=10))
+    rng = np.random.default_rng(31)
+    lens = rng.integers(0, 20, 4000).astype(np.uint64)
+    lens[[7, 1999, 3998]] = long_lens
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    ev = rng.integers(1, ds.catalogue_size + 1, int(off[-1])).astype(np.uint32)
+    big = dataclasses.replace(ds, trial_offsets=off, events=ev)
+    want = oracle.run_analysis(big, n_threads=8)
+    ctx = make_ctx(big, stream)
+    for flags in (ara.ARA_RUN_SYNC | ara.ARA_RUN_VALIDATE, ara.ARA_RUN_SYNC | ara.ARA_RUN_BALANCE,
+                  ara.ARA_RUN_SYNC | ara.ARA_RUN_HOIST):
+        assert_bit_identical(gpu_ylt(big, stream, ctx=ctx, flags=flags), want)
+    ctx.close()
+
+
 @pytest.mark.parametrize("preset,kw", [("tiny", dict(n_trials=700, k_min=0, k_max=45)),
                                        ("portfolio", dict(n_trials=300, k_min=20, k_max=90)),
                                        ("medium", dict(n_trials=600, k_min=1000, k_max=1000))])
