@@ -447,6 +447,21 @@ def test_metrics_parity(stream, n):
     ctx.close()
 
 
+def test_metrics_8m_entries_extreme_p(stream):
+    """The weak-scaling N = 8 metrics input (8M entries: rounded, 30% zeros, so heavy ties) at
+    probabilities next to 0 and 1 and on the rank boundaries k/n: PML exact, TVaR 1e-9."""
+    n = 8_000_000
+    rng = np.random.default_rng(8)
+    v = np.round(rng.exponential(1e6, n), 0) * (rng.random(n) < 0.7)
+    ps = [1e-12, 1e-7, 1 / n, 0.5, 1 - 1 / n, 1 - 1e-7, 1 - 1e-12, 0.999, 0.996]
+    ctx = ara.Context(0, stream)
+    pml, tvar = ctx.ara_metrics(torch.from_numpy(v).to(DEV), ps)
+    opml, otvar = oracle.metrics(v, ps)
+    assert np.array_equal(pml, opml)
+    assert np.allclose(tvar, otvar, rtol=1e-9, atol=0)
+    ctx.close()
+
+
 def test_metrics_ties_constant_and_zeros(stream):
     ctx = ara.Context(0, stream)
     for v in (np.zeros(1000), np.full(513, 3.25), np.repeat([0.0, 1.0, 2.0, 2.0, 5.0], 200),
