@@ -878,10 +878,14 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
         if (!h_trial_offsets || !h_ylt) return fail(ctx, ARA_ERR_ARG, "host pointer is NULL");
         const uint64_t ld = ylt_ld ? ylt_ld : n_trials;
         if (ld < n_trials) return fail(ctx, ARA_ERR_ARG, "ylt_ld < n_trials");
-        for (uint64_t t = 0; t < n_trials; ++t)
+        // one pass over the offsets: monotonicity and the longest trial (sizes the staging)
+        uint64_t max_trial = 0;
+        for (uint64_t t = 0; t < n_trials; ++t) {
             if (h_trial_offsets[t + 1] < h_trial_offsets[t])
                 return fail(ctx, ARA_ERR_VALIDATION, "trial offsets decrease at trial %llu",
                             (unsigned long long)t);
+            max_trial = std::max<uint64_t>(max_trial, h_trial_offsets[t + 1] - h_trial_offsets[t]);
+        }
         const uint64_t base = h_trial_offsets[0];
         if (h_trial_offsets[n_trials] > base && !h_event_ids)
             return fail(ctx, ARA_ERR_ARG, "h_event_ids is NULL");
@@ -903,9 +907,6 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
         }
         // chunking at trial boundaries: ~64 MiB of ids per chunk (>= 1 trial)
         const size_t kChunkIds = (size_t)16 << 20;
-        uint64_t max_trial = 0;
-        for (uint64_t t = 0; t < n_trials; ++t)
-            max_trial = std::max<uint64_t>(max_trial, h_trial_offsets[t + 1] - h_trial_offsets[t]);
         const size_t ids_cap = std::max<size_t>(kChunkIds, max_trial);
         const size_t off_cap = ids_cap + 2;  // a chunk holds at most ids_cap non-empty trials...
         if (ctx->ids_stage_cap < ids_cap || ctx->off_stage_cap < off_cap) {
