@@ -50,9 +50,10 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, variant: str = "",
-          defines: tuple = ()) -> str:
-    """Build libara.so; ``variant`` + ``defines`` build a tuning library libara_<variant>.so
-    with extra -D flags (loaded by the binding when ARA_LIB_VARIANT=<variant>)."""
+          defines: tuple = (), extra: tuple = ()) -> str:
+    """Build libara.so; ``variant`` + ``defines`` (+ ``extra`` nvcc flags for the kernel files)
+    build a tuning library libara_<variant>.so (loaded by the binding when
+    ARA_LIB_VARIANT=<variant>)."""
     lib = LIB if not variant else os.path.join(PKG, f"libara_{variant}.so")
     if not variant and not force and not _stale():
         return LIB
@@ -61,8 +62,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
     for src in _sources():  # the translation units compile in parallel
         name = os.path.basename(src)
         obj = os.path.join(BUILD, (f"{variant}_" if variant else "") + name + ".o")
-        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], *PER_FILE[name], "-c", src,
-               "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], *PER_FILE[name], *extra,
+               "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, *COMMON, *[f"-D{d}" for d in defines], "-x", "cu", *ARCH, "-c", src,
                    "-o", obj]
@@ -88,8 +89,10 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
 
 
 if __name__ == "__main__":
-    # python -m paper_1308_2572_b200.build [--force] [-v] [--variant NAME -DFOO=1 ...]
+    # python -m paper_1308_2572_b200.build [--force] [-v] [--variant NAME -DFOO=1 ...
+    #                                      --nvcc=-maxrregcount=144 ...]
     a = sys.argv[1:]
     var = a[a.index("--variant") + 1] if "--variant" in a else ""
     print(build(force="--force" in a, verbose="-v" in a, variant=var,
-                defines=tuple(x[2:] for x in a if x.startswith("-D"))))
+                defines=tuple(x[2:] for x in a if x.startswith("-D")),
+                extra=tuple(x[7:] for x in a if x.startswith("--nvcc="))))
