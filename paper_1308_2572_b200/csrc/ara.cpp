@@ -256,8 +256,9 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     // equal lengths, profiles/README.md).  When the previous run's trials were all equally long
     // the sort is skipped (identity order; a cheap check keeps the verdict current).
     // ARA_SCAN_SCHED=static|dynamic selects the plain round-robin / per-group ticket schedules
-    // (tuning); the F4 outputs use per-group tickets.
-    const bool balance = ctx->sched == 0 && !extra && n <= 0xffffffffull;  // u32 permutation
+    // (tuning); the F4 outputs of an fp32 store use per-group tickets.
+    const bool balance = ctx->sched == 0 && (!extra || ctx->store.bits == 64) &&
+                         n <= 0xffffffffull;  // u32 permutation
     const bool sorted = balance && !ctx->lengths_equal;
     const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
     const uint32_t *perm = nullptr;

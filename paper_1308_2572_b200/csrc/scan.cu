@@ -100,13 +100,13 @@ __device__ __forceinline__ void event_step(const Chunk<R> (&r)[CH],
 
 // F4 outputs of one event (X: compiled in only when requested): the trial's maximum
 // occurrence loss and the event's incremental aggregate loss at its YET position.
-template <bool X, typename R>
+template <int X, typename R>
 __device__ __forceinline__ void event_out(R oc, R inc, R &max_oc, double *inc_row, uint64_t pos,
                                           bool writer)
 {
     if (X) {
         max_oc = (max_oc < oc) ? oc : max_oc;
-        if (inc_row && writer) inc_row[pos] = (double)inc;
+        if (X == 2 && inc_row && writer) inc_row[pos] = (double)inc;
     }
 }
 
@@ -127,7 +127,7 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
 #endif
 }
 
-template <int G, int CH, bool X, typename R, bool BAL, int MM, int D>
+template <int G, int CH, int X, typename R, bool BAL, int MM, int D>
 __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
                                           const uint32_t *__restrict__ bitmap,
                                           const R *__restrict__ rows,
@@ -195,7 +195,8 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
             ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
             if (X) {
                 mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
-                inc_row = s.event_inc ? s.event_inc + (size_t)layer * s.event_inc_ld : nullptr;
+                inc_row = X == 2 && s.event_inc ? s.event_inc + (size_t)layer * s.event_inc_ld
+                                                : nullptr;
             }
             cur_layer = layer;
         }
@@ -333,7 +334,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
 
 // The kernel: map mode 2 runs its mode-1 body when the hit probe found (nearly) every sampled
 // id in the store (probe_use_bitmap), chosen once per launch.
-template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D = 2>
+template <int G, int CH, int MINB, int X, typename R, bool BAL, int MM, int D = 2>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                 const uint32_t *__restrict__ bitmap, const R *__restrict__ rows,
@@ -411,7 +412,7 @@ __global__ void length_keys_kernel(const uint64_t *__restrict__ offsets, uint64_
     if (differ && __any_sync(0xffffffffu, d) && (threadIdx.x & 31u) == 0) atomicOr(differ, 1ull);
 }
 
-template <int G, int CH, int MINB, bool X, typename R, bool BAL, int MM, int D>
+template <int G, int CH, int MINB, int X, typename R, bool BAL, int MM, int D>
 cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                        cudaStream_t stream)
 {
@@ -456,7 +457,7 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
 }
 
 // Map mode dispatch.
-template <int G, int CH, int MINB = 1, bool X = false, typename R = double, bool BAL = false,
+template <int G, int CH, int MINB = 1, int X = 0, typename R = double, bool BAL = false,
           int D = 2>
 cudaError_t launch_gc(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                       cudaStream_t stream)
@@ -522,70 +523,88 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
 {
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
-    if (s.perm && !(s.max_occ || s.event_inc)) {  // length-bucketed (ARA_RUN_BALANCE)
+    if (s.perm && (s.max_occ || s.event_inc)) {  // F4 outputs, length-bucketed (fp64 store)
+        if (st.bits != 64) { --*launches; return cudaErrorInvalidValue; }
+        // X = 1: the per-trial maximum only (no increment code in the loop); X = 2: both
+        const bool inc = s.event_inc != nullptr;
+        switch (st.width) {
+#define ARA_F4_BAL(G_, CH_, MINB_)                                                          \
+    return inc ? launch_gc<G_, CH_, MINB_, 2, double, true>(st, s, sm_count, stream)        \
+               : launch_gc<G_, CH_, MINB_, 1, double, true>(st, s, sm_count, stream)
+            case 4: ARA_F4_BAL(1, 1, 1);
+            case 8: ARA_F4_BAL(2, 1, 4);
+            case 16: ARA_F4_BAL(2, 2, 3);
+            case 32: ARA_F4_BAL(4, 2, 3);
+            case 48: ARA_F4_BAL(4, 3, 1);
+            case 64: ARA_F4_BAL(4, 4, 1);
+#undef ARA_F4_BAL
+            default: --*launches; return cudaErrorInvalidValue;
+        }
+    }
+    if (s.perm) {  // length-bucketed (ARA_RUN_BALANCE)
         if (st.bits == 32) {
             switch (st.width) {
                 // register caps (__launch_bounds__ min blocks): without them ptxas spends up to
                 // 254 registers on deeper pipelining and halves the resident warps
-                case 8: return launch_gc<1, 1, 4, false, float, true>(st, s, sm_count, stream);
-                case 16: return launch_gc<2, 1, 4, false, float, true>(st, s, sm_count, stream);
-                case 32: return launch_gc<2, 2, 2, false, float, true>(st, s, sm_count, stream);
-                case 64: return launch_gc<4, 2, 2, false, float, true>(st, s, sm_count, stream);
+                case 8: return launch_gc<1, 1, 4, 0, float, true>(st, s, sm_count, stream);
+                case 16: return launch_gc<2, 1, 4, 0, float, true>(st, s, sm_count, stream);
+                case 32: return launch_gc<2, 2, 2, 0, float, true>(st, s, sm_count, stream);
+                case 64: return launch_gc<4, 2, 2, 0, float, true>(st, s, sm_count, stream);
                 default: --*launches; return cudaErrorInvalidValue;
             }
         }
         switch (st.width) {
-            case 4: return launch_gc<1, 1, 1, false, double, true>(st, s, sm_count, stream);
-            case 8: return launch_gc<2, 1, 4, false, double, true>(st, s, sm_count, stream);
+            case 4: return launch_gc<1, 1, 1, 0, double, true>(st, s, sm_count, stream);
+            case 8: return launch_gc<2, 1, 4, 0, double, true>(st, s, sm_count, stream);
             case 16:  // tuning variants: ARA_SCAN_GROUP (G), ARA_SCAN_DEPTH (D), ARA_SCAN_MINB
                 if (st.group_override == 4) {
                     if (st.depth == 8)
-                        return launch_gc<4, 1, 3, false, double, true, 8>(st, s, sm_count, stream);
+                        return launch_gc<4, 1, 3, 0, double, true, 8>(st, s, sm_count, stream);
                     if (st.min_blocks == 4)
-                        return launch_gc<4, 1, 4, false, double, true, 4>(st, s, sm_count, stream);
-                    return launch_gc<4, 1, 3, false, double, true, 4>(st, s, sm_count, stream);
+                        return launch_gc<4, 1, 4, 0, double, true, 4>(st, s, sm_count, stream);
+                    return launch_gc<4, 1, 3, 0, double, true, 4>(st, s, sm_count, stream);
                 }
                 if (st.depth == 4 && st.min_blocks == 3)
-                    return launch_gc<2, 2, 3, false, double, true, 4>(st, s, sm_count, stream);
+                    return launch_gc<2, 2, 3, 0, double, true, 4>(st, s, sm_count, stream);
                 if (st.depth == 4)
-                    return launch_gc<2, 2, 2, false, double, true, 4>(st, s, sm_count, stream);
+                    return launch_gc<2, 2, 2, 0, double, true, 4>(st, s, sm_count, stream);
                 if (st.min_blocks == 2)
-                    return launch_gc<2, 2, 2, false, double, true>(st, s, sm_count, stream);
-                return launch_gc<2, 2, 3, false, double, true>(st, s, sm_count, stream);
+                    return launch_gc<2, 2, 2, 0, double, true>(st, s, sm_count, stream);
+                return launch_gc<2, 2, 3, 0, double, true>(st, s, sm_count, stream);
             case 32:
                 if (st.group_override == 8)
-                    return launch_gc<8, 1, 4, false, double, true>(st, s, sm_count, stream);
-                return launch_gc<4, 2, 3, false, double, true>(st, s, sm_count, stream);
-            case 48: return launch_gc<4, 3, 1, false, double, true>(st, s, sm_count, stream);
+                    return launch_gc<8, 1, 4, 0, double, true>(st, s, sm_count, stream);
+                return launch_gc<4, 2, 3, 0, double, true>(st, s, sm_count, stream);
+            case 48: return launch_gc<4, 3, 1, 0, double, true>(st, s, sm_count, stream);
             case 64:
                 if (st.group_override == 8)
-                    return launch_gc<8, 2, 3, false, double, true>(st, s, sm_count, stream);
-                return launch_gc<4, 4, 1, false, double, true>(st, s, sm_count, stream);
+                    return launch_gc<8, 2, 3, 0, double, true>(st, s, sm_count, stream);
+                return launch_gc<4, 4, 1, 0, double, true>(st, s, sm_count, stream);
             default: --*launches; return cudaErrorInvalidValue;
         }
     }
     if (st.bits == 32) {  // F3: fp32 store (widths in floats: 8, 16, 32, 64)
         const bool x = s.max_occ || s.event_inc;
         switch (st.width) {
-            case 8: return x ? launch_gc<1, 1, 1, true, float>(st, s, sm_count, stream)
-                             : launch_gc<1, 1, 1, false, float>(st, s, sm_count, stream);
-            case 16: return x ? launch_gc<2, 1, 1, true, float>(st, s, sm_count, stream)
-                              : launch_gc<2, 1, 1, false, float>(st, s, sm_count, stream);
-            case 32: return x ? launch_gc<2, 2, 1, true, float>(st, s, sm_count, stream)
-                              : launch_gc<2, 2, 1, false, float>(st, s, sm_count, stream);
-            case 64: return x ? launch_gc<4, 2, 1, true, float>(st, s, sm_count, stream)
-                              : launch_gc<4, 2, 1, false, float>(st, s, sm_count, stream);
+            case 8: return x ? launch_gc<1, 1, 1, 2, float>(st, s, sm_count, stream)
+                             : launch_gc<1, 1, 1, 0, float>(st, s, sm_count, stream);
+            case 16: return x ? launch_gc<2, 1, 1, 2, float>(st, s, sm_count, stream)
+                              : launch_gc<2, 1, 1, 0, float>(st, s, sm_count, stream);
+            case 32: return x ? launch_gc<2, 2, 1, 2, float>(st, s, sm_count, stream)
+                              : launch_gc<2, 2, 1, 0, float>(st, s, sm_count, stream);
+            case 64: return x ? launch_gc<4, 2, 1, 2, float>(st, s, sm_count, stream)
+                              : launch_gc<4, 2, 1, 0, float>(st, s, sm_count, stream);
             default: --*launches; return cudaErrorInvalidValue;
         }
     }
-    if (s.max_occ || s.event_inc) {  // F4 outputs: default decomposition only
+    if (s.max_occ || s.event_inc) {  // F4 outputs, per-group tickets (fp32 store, > 2^32 trials)
         switch (st.width) {
-            case 4: return launch_gc<1, 1, 1, true>(st, s, sm_count, stream);
-            case 8: return launch_gc<2, 1, 1, true>(st, s, sm_count, stream);
-            case 16: return launch_gc<2, 2, 3, true>(st, s, sm_count, stream);
-            case 32: return launch_gc<4, 2, 1, true>(st, s, sm_count, stream);
-            case 48: return launch_gc<4, 3, 1, true>(st, s, sm_count, stream);
-            case 64: return launch_gc<4, 4, 1, true>(st, s, sm_count, stream);
+            case 4: return launch_gc<1, 1, 1, 2>(st, s, sm_count, stream);
+            case 8: return launch_gc<2, 1, 1, 2>(st, s, sm_count, stream);
+            case 16: return launch_gc<2, 2, 3, 2>(st, s, sm_count, stream);
+            case 32: return launch_gc<4, 2, 1, 2>(st, s, sm_count, stream);
+            case 48: return launch_gc<4, 3, 1, 2>(st, s, sm_count, stream);
+            case 64: return launch_gc<4, 4, 1, 2>(st, s, sm_count, stream);
             default: --*launches; return cudaErrorInvalidValue;
         }
     }
