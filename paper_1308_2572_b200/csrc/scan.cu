@@ -110,6 +110,56 @@ __device__ __forceinline__ void event_out(R oc, R inc, R &max_oc, double *inc_ro
     }
 }
 
+// F4 increments of an aligned 8-event chunk (X == 2, the pipelined loop): the writer lane
+// stages inc_d in shared memory and the group stores the chunk's 8 increments as one 64-byte
+// segment (one full 32-byte sector per lane for G = 2) instead of 8 scattered 8-byte stores.
+template <int X, typename R>
+__device__ __forceinline__ void event_out_staged(R oc, R inc, R &max_oc, double *stage, int j,
+                                                 bool writer)
+{
+    max_oc = (max_oc < oc) ? oc : max_oc;
+    if (X == 2 && stage && writer) stage[j] = (double)inc;
+}
+
+__device__ __forceinline__ void store_v2(double *p, double a, double b)
+{
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ void store_v4(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+                 "d"(d)
+                 : "memory");
+}
+
+template <int G>
+__device__ __forceinline__ void flush_inc(const double *stage, double *dst, uint32_t c,
+                                          uint32_t gmask)
+{
+    constexpr int PER = 8 / G;  // increments stored by each lane of the group
+    __syncwarp(gmask);          // the writer's staged values are visible to the group
+    const double *src = stage + c * PER;
+    double *d = dst + c * PER;
+    if ((((uintptr_t)dst) & 63u) == 0) {
+        if constexpr (PER == 8) {
+            store_v4(d, src[0], src[1], src[2], src[3]);
+            store_v4(d + 4, src[4], src[5], src[6], src[7]);
+        } else if constexpr (PER == 4) {
+            store_v4(d, src[0], src[1], src[2], src[3]);
+        } else if constexpr (PER == 2) {
+            store_v2(d, src[0], src[1]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) d[k] = src[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) d[k] = src[k];
+    }
+    __syncwarp(gmask);  // the stage is read before the next chunk overwrites it
+}
+
 template <int CH, typename R>
 __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t stride,
                                        uint32_t idx, Chunk<R> (&r)[CH])
@@ -136,6 +186,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
+    __shared__ __align__(16) double s_inc[X == 2 ? (kScanThreads / G) * 8 : 2];  // F4 staging
     constexpr int PER = Chunk<R>::N;
     constexpr int W = PER * G * CH;  // row width per layer (elements)
     constexpr int NCOL = PER * CH;   // columns per lane
@@ -256,6 +307,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                 ev += 8 * n_chunks;
             }
         } else if (n_chunks) {
+            double *const stage = (X == 2 && inc_row) ? s_inc + (threadIdx.x / G) * 8 : nullptr;
             uint32_t id_c[8], id_n[8];
             load_ids8(ev, id_c);
             if (n_chunks > 1) load_ids8(ev + 8, id_n);
@@ -277,14 +329,23 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                     gather<CH, R>(my_rows, row_stride, pin(idx1, own), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc, own);
-                    event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
+                    if constexpr (X == 2)
+                        event_out_staged<X, R>(oc, inc, max_oc, stage, j, writer);
+                    else
+                        event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                     uint32_t idx3 = ok2 ? row_index<MM>(look, id3, bad) : zb;
                     gather<CH, R>(my_rows, row_stride, pin(idx2, own), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc, own);
-                    event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1, writer);
+                    if constexpr (X == 2)
+                        event_out_staged<X, R>(oc, inc, max_oc, stage, j + 1, writer);
+                    else
+                        event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j + 1,
+                                        writer);
                     idx1 = idx3;
                 }
+                if constexpr (X == 2)
+                    if (stage) flush_inc<G>(stage, inc_row + (ev - s.ids) + 8 * i, c, gmask);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
                 if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
