@@ -81,12 +81,41 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
+    # NVML clock-event reason bits (the values nvidia-smi's clocks_event_reasons.* report)
+    NVML_REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                    0x4: "sw_power_cap"}
+
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = f"/tmp/ara_clocks_{os.getpid()}.csv"
+        self.nvml_rows = []
+        self.thread = None
+
+    def _nvml_poll(self):
+        # nvidia-smi needs ~100 ms to start, about half a timed region: NVML (the library behind
+        # nvidia-smi) is also polled every 10 ms from a thread
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self.stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = (pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons")
+                        else pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
+                self.nvml_rows.append((float(sm), float(mx), bits))
+                self.stop.wait(0.01)
+            pynvml.nvmlShutdown()
+        except Exception:
+            pass
 
     def __enter__(self):
+        import threading
+        self.stop = threading.Event()
+        self.thread = threading.Thread(target=self._nvml_poll, daemon=True)
+        self.thread.start()
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -98,6 +127,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
@@ -107,7 +139,9 @@ class ClockSampler:
             self.f.close()
 
     def summary(self):
-        if not self.proc:
+        nv = [(sm, mx, sorted(n for b, n in self.NVML_REASONS.items() if bits & b))
+              for sm, mx, bits in self.nvml_rows]
+        if not self.proc and not nv:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         rows = []
         for line in open(self.path):
@@ -118,13 +152,17 @@ class ClockSampler:
                 rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = [(sm, mx, [names[i] for i, v in enumerate(r) if v.lower() == "active"])
+                for sm, mx, r in rows]
+        smi_n = len(rows)
+        rows += nv
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r)
-                          if v.lower() == "active"})
+        reasons = sorted({x for _, _, r in rows for x in r})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": rows[0][1],
-                "samples": len(rows), "reasons": reasons}
+                "samples": len(rows), "samples_nvidia_smi": smi_n, "samples_nvml": len(nv),
+                "reasons": reasons}
 
 
 def cpu_baseline_measure(spec, ds_host_elts, target_s: float = 15.0, per_core: bool = True):
