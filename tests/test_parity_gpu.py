@@ -654,6 +654,35 @@ def test_f4_outputs(stream, preset, kw):
     ctx.close()
 
 
+@pytest.mark.parametrize("n_elts", [1, 5, 8, 24, 33, 48, 64])
+@pytest.mark.parametrize("sched", ["", "dynamic"])
+def test_f4_outputs_widths(stream, monkeypatch, n_elts, sched):
+    """F4 at every row width class (one, two and four lanes per trial; the increments of an
+    aligned 8-event chunk are stored as one 64-byte segment by 1, 2 or 4 lanes) in both
+    schedules (length-bucketed warp batches; per-group tickets), 3 layers with 64-byte aligned
+    increment rows, against the oracle bit for bit."""
+    if sched:
+        monkeypatch.setenv("ARA_SCAN_SCHED", sched)
+    spec = datagen.PRESETS["portfolio"].replace(n_elts=n_elts, elts_per_layer=n_elts,
+                                                n_layers=3, layer_stride=0, n_trials=500,
+                                                k_min=0, k_max=70, seed=40 + n_elts)
+    ds = datagen.generate(spec)
+    y_o, mo_o, inc_o = oracle.run_analysis(ds, n_threads=8, outputs=True)
+    ctx = make_ctx(ds, stream)
+    L, n = ds.n_layers, ds.n_trials
+    n_ev = int(ds.trial_offsets[-1])
+    ld = (n_ev + 7) // 8 * 8
+    ylt = torch.full((L, n), float("nan"), dtype=torch.float64, device=DEV)
+    mo = torch.full((L, n), float("nan"), dtype=torch.float64, device=DEV)
+    inc = torch.full((L, ld), float("nan"), dtype=torch.float64, device=DEV)
+    ctx.ara_run_outputs(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt, mo, inc,
+                        flags=ara.ARA_RUN_SYNC, event_inc_ld=ld)
+    assert_bit_identical(ylt.cpu().numpy(), y_o)
+    assert_bit_identical(mo.cpu().numpy(), mo_o)
+    assert_bit_identical(inc.cpu().numpy()[:, :n_ev], inc_o)
+    ctx.close()
+
+
 # --------------------------------------------------------------------------- F3 (fp32)
 def make_ctx32(ds, stream):
     ctx = ara.Context(0, stream)
