@@ -144,7 +144,7 @@ class ClockSampler:
         if not self.proc and not nv:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         rows = []
-        for line in open(self.path):
+        for line in (open(self.path) if self.proc else ()):
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue

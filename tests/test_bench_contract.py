@@ -43,6 +43,21 @@ def test_partition_matches_dist():
         assert [bench.partition(n, r, R) for r in range(R)] == partition_trials(n, R)
 
 
+def test_clock_summary_reasons():
+    """The clocks line merges nvidia-smi and NVML samples; throttle reasons are named from
+    either source (a run that saw hw/thermal slowdowns must say so)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    cs = bench.ClockSampler(0)
+    cs.nvml_rows = [(1965.0, 1965.0, 0), (1900.0, 1965.0, 0x4), (1965.0, 1965.0, 0x8 | 0x40)]
+    s = cs.summary()
+    assert s["samples"] == 3 and s["samples_nvml"] == 3 and s["samples_nvidia_smi"] == 0
+    assert s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["hw_slowdown", "hw_thermal_slowdown", "sw_power_cap"]
+    empty = bench.ClockSampler(0).summary()
+    assert empty["sm_mhz"] is None and empty["reasons"]
+
+
 @pytest.mark.gpu
 def test_bench_json_line_on_gpu():
     """bench.py on the GPU (medium config, short run) prints one JSON line with every key the
