@@ -92,30 +92,37 @@ class ClockSampler:
         self.nvml_rows = []
         self.thread = None
 
+    def _nvml_sample(self):
+        import pynvml
+        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        bits = (pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons")
+                else pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+        self.nvml_rows.append((float(sm), float(self.mx), bits))
+
     def _nvml_poll(self):
         # nvidia-smi needs ~100 ms to start, about half a timed region: NVML (the library behind
-        # nvidia-smi) is also polled every 10 ms from a thread
+        # nvidia-smi) is also polled every 10 ms from a thread, and sampled once more when the
+        # region ends (short regions)
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self.stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                bits = (pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        if hasattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons")
-                        else pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h))
-                self.nvml_rows.append((float(sm), float(mx), bits))
-                self.stop.wait(0.01)
-            pynvml.nvmlShutdown()
+            while not self.stop.wait(0.01):
+                self._nvml_sample()
         except Exception:
             pass
 
     def __enter__(self):
         import threading
         self.stop = threading.Event()
-        self.thread = threading.Thread(target=self._nvml_poll, daemon=True)
-        self.thread.start()
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._nvml_poll, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.h = None
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -130,6 +137,13 @@ class ClockSampler:
         self.stop.set()
         if self.thread:
             self.thread.join(timeout=5)
+        if self.h is not None:
+            try:
+                self._nvml_sample()
+                import pynvml
+                pynvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -142,7 +156,8 @@ class ClockSampler:
         nv = [(sm, mx, sorted(n for b, n in self.NVML_REASONS.items() if bits & b))
               for sm, mx, bits in self.nvml_rows]
         if not self.proc and not nv:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0,
+                    "reasons": ["nvidia-smi unavailable"]}
         rows = []
         for line in (open(self.path) if self.proc else ()):
             parts = [x.strip() for x in line.split(",")]
@@ -158,7 +173,7 @@ class ClockSampler:
         smi_n = len(rows)
         rows += nv
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0, "reasons": ["no samples"]}
         reasons = sorted({x for _, _, r in rows for x in r})
         return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": rows[0][1],
                 "samples": len(rows), "samples_nvidia_smi": smi_n, "samples_nvml": len(nv),
