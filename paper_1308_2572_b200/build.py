@@ -28,6 +28,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-fno-fast-m
 # explicitly); the oracle's reading R7 fixes separately rounded products and differences.
 PER_FILE = {
     "scan.cu": ["-fmad=false", "-Xptxas", "-v"],
+    "scan_pair.cu": ["-fmad=false", "-Xptxas", "-v"],
     "portfolio.cu": ["-fmad=false", "-Xptxas", "-v"],
     "hoist.cu": ["-fmad=false", "-Xptxas", "-v"],
     "metrics.cu": ["-Xptxas", "-v"],

@@ -5,6 +5,8 @@
 // and orchestration of the scan (A2-A8) and metrics (A9) kernels on the context stream.
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <cmath>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -311,7 +313,9 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
             : st1.uni.enabled
                 ? ara::launch_portfolio(st1.uni, st1.d_map, 1, st1.d_bitmap, s, ctx->sm_count,
                                         ctx->stream, &ctx->launches)
-                : ara::launch_scan(st1, s, ctx->sm_count, ctx->stream, &ctx->launches);
+                : ara::pair_scan_eligible(st1, s)
+                    ? ara::launch_pair_scan(st1, s, ctx->sm_count, ctx->stream, &ctx->launches)
+                    : ara::launch_scan(st1, s, ctx->sm_count, ctx->stream, &ctx->launches);
     } else {
         e = hoist ? ara::launch_hoisted_scan(ctx->store, s, ctx->sm_count, ctx->stream,
                                              &ctx->launches)
@@ -319,7 +323,10 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                 ? ara::launch_portfolio(ctx->store.uni, ctx->store.d_map, ctx->store.map_mode,
                                         ctx->store.d_bitmap, s, ctx->sm_count, ctx->stream,
                                         &ctx->launches)
-                : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
+                : ara::pair_scan_eligible(ctx->store, s)
+                    ? ara::launch_pair_scan(ctx->store, s, ctx->sm_count, ctx->stream,
+                                            &ctx->launches)
+                    : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     return ARA_OK;
@@ -360,6 +367,31 @@ void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vecto
         lt[l].agg_ret = (R)terms[l].agg_retention;
         lt[l].agg_lim = (R)terms[l].agg_limit;
     }
+}
+
+// scan_pair.cu carries 2^m multiples of the oracle's values (exact scaled clamps); this bounds
+// every input magnitude it scales: each record's loss * rate (rounded up), each retention and
+// finite limit, each layer term.  With all of them below 2^960 no scaled intermediate of a trial
+// of k < 2^36 events over E <= 64 ELTs can overflow (8 (k (E + 1) + 1) 2^960 < 2^1023).
+bool scaled_terms_ok(const ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms *terms,
+                     const uint32_t *elt_offsets, const uint32_t *elt_index)
+{
+    const double bound = std::ldexp(1.0, 960);
+    auto ok = [&](double v) { return std::isinf(v) || v < bound; };  // +inf limits scale to +inf
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        const ara_layer_terms &t = terms[l];
+        if (!ok(t.occ_limit) || !ok(t.agg_limit) || !(t.occ_retention < bound) ||
+            !(t.agg_retention < bound))
+            return false;
+        for (uint32_t c = elt_offsets[l]; c < elt_offsets[l + 1]; ++c) {
+            const uint32_t j = elt_index[c];
+            const ara_fin_terms &f = ctx->fin[j];
+            if (!(f.retention < bound) || !(f.rate < bound) || !ok(f.limit)) return false;
+            for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
+                if (!(ctx->rec_losses[r] * f.rate * 1.0000001 < bound)) return false;
+        }
+    }
+    return true;
 }
 
 // F1 union-row store (portfolio.cu) when the portfolio qualifies; returns ARA_OK either way
@@ -746,6 +778,12 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
         if (const char *d = getenv("ARA_SCAN_DEPTH")) st.depth = atoi(d);
+        if (const char *q = getenv("ARA_PAIR_SCAN")) {
+            st.pair_scan = atoi(q) != 0;
+            st.pair_scan_wide = atoi(q) == 2;
+        }
+        st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
+                                                       elt_index);
         std::vector<uint32_t> map((size_t)C + 1, 0u);
         std::vector<uint32_t> uni;
         for (uint32_t c = elt_offsets[0]; c < elt_offsets[n_layers]; ++c) {

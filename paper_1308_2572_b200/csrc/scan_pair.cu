@@ -1,0 +1,402 @@
+// scan_pair.cu -- the fp64 YET scan (Algorithm 1 lines 3-29) for sm_100a on
+// rows of W = 16, 32 or 64 columns: pair-skewed lane groups and exactly scaled clamps.
+//
+// Decomposition.  A row of W = 16 P doubles is P 128-byte lines.  A group of G = 2 P lanes owns
+// one (trial, layer) ticket; lane c owns the 8 columns [8c, 8c + 8) of the layer's row (two
+// 256-bit loads), so pair p = (lanes 2p, 2p + 1) covers line p and each of its load instructions
+// touches one line per pair -- the same L1 wavefront cost per line as the 16-column kernel.  The
+// ELT sum of lines 11-13 must be the oracle's ((0 + F_0) + F_1) + ... + F_{W-1} (SURVEY.md
+// finding 3), i.e. a chain through the lanes in column order.  Pair p works one event behind
+// pair p - 1 ("skew"): at step s lane c processes event s - floor(c / 2), so in every step
+// phase A (even lanes: the first 8 columns of their line) and phase B (odd lanes: the last 8,
+// continuing from the even lane's partial) all P pairs advance their own event in the same two
+// phases.  The partial of event e leaves pair p at the end of step s and enters pair p + 1 at
+// step s + 1, when pair p + 1 has event e's line in its registers.  Per step the group issues
+// 16 ordered adds per lane whatever P is (the unskewed chain needs 8 P), and the loads of a step
+// touch P lines -- one per pair -- exactly as without the skew.  The row index of pair p at step
+// s is pair p - 1's index at step s - 1 (one shuffle); a trial takes k + P - 1 steps, the first
+// and last P - 1 of them reading zero rows on the idle pairs (exact no-ops, reading R12).
+//
+// Exactly scaled clamps.  sm_100a has no fp64 min/max instruction; max(x, 0) as a compare-select
+// costs DSETP + 2 FSEL.  Instead the kernel carries power-of-two multiples of the oracle's values:
+//   2 max(x, 0) = x + |x|  exactly (x > 0: 2x is exact; x <= 0: x + |x| = +0 under RN),
+// and scaling by 2^m commutes with every RN add/sub/compare as long as nothing overflows (sums of
+// subnormals are exact, so underflow cannot differ either).  Per event:
+//   F2_j  = min(x_j + |x_j|, 2 lim_j)                       = 2 F_j      (line 9)
+//   lo2   = ((F2_0 + F2_1) + ...)                           = 2 lo      (lines 11-13)
+//   t2    = lo2 - 2 OccR;  oc4 = min(t2 + |t2|, 4 OccL)     = 4 oc      (line 16)
+//   S4   += oc4                                             = 4 S       (line 19)
+//   u4    = S4 - 4 AggR;   C8  = min(u4 + |u4|, 8 AggL)     = 8 C_d     (line 22)
+//   inc8  = C8 - C8_prev;  lr8 += inc8                      = 8 lr      (lines 25, 28)
+// and the YLT entry is lr8 * 0.125 (exact).  ara_set_layers enables this path only when every
+// loss * rate, retention, finite limit and layer term is below 2^960, so that 8 (k (E + 1) + 1)
+// times that bound cannot overflow for any YET the device can hold (k < 2^36, E <= 64); other
+// portfolios run scan.cu's compare-select kernel.  The result is bit-identical to the oracle's
+// unscaled sequence (tests/test_parity_gpu.py).  (0 + F_0 = F_0 for F_0 >= +0, and F2 is never
+// -0, so the chain may start at F2_0.)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "ara_internal.h"
+#include "scan_common.cuh"
+
+namespace ara {
+namespace {
+
+using namespace scan_detail;
+
+constexpr unsigned kFull = 0xffffffffu;
+
+struct ScaledTerms {
+    double rate[8], ret[8], lim2[8];  // this lane's columns
+    double occ_ret2, occ_lim4, agg_ret4, agg_lim8;
+};
+
+// 2 max(x, 0), exact (see the file comment)
+__device__ __forceinline__ double twice_max0(double x) { return __dadd_rn(x, fabs(x)); }
+
+// max(x, 0) on the integer pipe (sign mask; -0 -> +0): the columns j < ARA_PAIR_INTMAX compute
+// x2 = l (2 rate) - 2 ret = 2 x exactly (power-of-two scaled terms) and clear it when negative,
+// moving one fp64 operation per column to the ALU (tuning; default 0)
+#ifndef ARA_PAIR_INTMAX
+#define ARA_PAIR_INTMAX 0
+#endif
+__device__ __forceinline__ double int_max0(double x)
+{
+    const int hi = __double2hiint(x), lo = __double2loint(x);
+    const int keep = ~(hi >> 31);
+    return __hiloint2double(hi & keep, lo & keep);
+}
+__device__ __forceinline__ double cmin(double m, double lim) { return (lim < m) ? lim : m; }
+
+// Trial state of the group's last lane (lane G - 1 ends every step with the full ELT sum of its
+// event); the other lanes carry the same registers with meaningless values.
+struct TrialState {
+    double S4, C8, lr8, max4;
+};
+
+// One step of lane c on its row segment r (event s - c/2): financial terms of its 8 columns,
+// phase A / phase B of the ELT chain, then (meaningful in lane G - 1) the occurrence and
+// aggregate terms.  xB carries the lane's phase-B partial to the next step (P > 1); own is the
+// lane's phase-A value (the gather pin).  Returns inc8 (lane G - 1).
+template <int P>
+__device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
+                                            uint32_t c, uint32_t gmask, double &xB, double &own,
+                                            TrialState &st)
+{
+    constexpr int G = 2 * P;
+    double f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double x = rsub(rmul(r[j >> 2].v[j & 3], T.rate[j]), T.ret[j]);  // line 9
+        f[j] = cmin(j < ARA_PAIR_INTMAX ? int_max0(x) : twice_max0(x), T.lim2[j]);
+    }
+    double a;
+    if constexpr (P == 1) {  // lane 0 starts the chain at F2_0 (= 0 + F2_0)
+        a = f[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) a = radd(a, f[j]);
+    } else {  // even lane 2p > 0 continues event s - p from lane 2p - 1's last phase B
+        const double in = __shfl_up_sync(gmask, xB, 1, G);
+        a = (c == 0) ? 0.0 : in;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a = radd(a, f[j]);
+    }
+    own = a;
+    double b = __shfl_up_sync(gmask, a, 1, G);  // odd lane 2p + 1 continues lane 2p's partial
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b = radd(b, f[j]);
+    xB = b;
+    // lines 15-29 on lo2 = b (lane G - 1)
+    const double t2 = rsub(b, T.occ_ret2);
+    const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
+    st.S4 = radd(st.S4, oc4);
+    const double u4 = rsub(st.S4, T.agg_ret4);
+    const double C8 = cmin(twice_max0(u4), T.agg_lim8);
+    const double inc8 = rsub(C8, st.C8);
+    st.lr8 = radd(st.lr8, inc8);
+    st.C8 = C8;
+    st.max4 = (st.max4 < oc4) ? oc4 : st.max4;  // F4 (dead code unless stored)
+    return inc8;
+}
+
+__device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
+                                        uint32_t idx, Chunk<double> (&r)[2])
+{
+    const double *p = my_rows + (size_t)idx * stride;
+    load_row_chunk(p, r[0]);
+    load_row_chunk(p + 4, r[1]);
+}
+
+// Row index of this lane for the next step: pair 0 from its own event id, pair p > 0 takes pair
+// p - 1's index of the current step.
+template <int P>
+__device__ __forceinline__ uint32_t next_index(uint32_t idx0, uint32_t cur, uint32_t c,
+                                               uint32_t gmask)
+{
+    if constexpr (P == 1) {
+        (void)cur;
+        (void)c;
+        (void)gmask;
+        return idx0;
+    } else {
+        const uint32_t up = __shfl_up_sync(gmask, cur, 2, 2 * P);
+        return c < 2 ? idx0 : up;
+    }
+}
+
+template <int P, int MM, int X>
+__device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
+                                          const uint32_t *__restrict__ bitmap,
+                                          const double *__restrict__ rows,
+                                          const LayerTermsT<double> *__restrict__ terms,
+                                          uint32_t n_layers)
+{
+    extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
+    load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
+    constexpr int G = 2 * P;
+    constexpr uint32_t W = 16 * P;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t c = lane % G;
+    // group mask: the groups of a warp run different trials (ragged lengths, head/tail loops)
+    const uint32_t gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (lane - c));
+    const bool writer = c == G - 1;
+    const uint32_t B = 32 / G, gw = lane / G;  // groups per warp, this group's index in it
+    const uint64_t warp_g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) / 32;
+    const uint64_t n_tickets = s.n_trials * n_layers;
+    const uint32_t row_stride = n_layers * W;
+    const uint32_t zb = s.zero_base;
+    const RowLookup look{map, sbits, s.catalogue_size, zb, s.bitmap_log2};
+    const uint64_t base = s.offsets[0];
+
+    ScaledTerms T;
+    const double *__restrict__ my_rows = rows;
+    double *ylt_row = s.ylt, *mo_row = nullptr, *inc_row = nullptr;
+    uint32_t cur_layer = 0xffffffffu;
+    bool bad = false;
+
+    // Warp-batched tickets in length order (s.perm): ticket q = (trial perm[q / L], layer q % L);
+    // a warp takes B consecutive tickets at a time from the device counter.
+    for (uint64_t ticket = warp_g * B + gw;;) {
+        if (ticket - gw >= n_tickets) break;  // warp-uniform
+        if (ticket < n_tickets) {
+            const uint64_t q = ticket / n_layers;
+            const uint64_t t = s.perm ? (uint64_t)s.perm[q] : q;
+            const uint32_t layer = (uint32_t)(ticket - q * n_layers);
+            if (layer != cur_layer) {
+                const LayerTermsT<double> &L = terms[layer];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {  // int_max0 columns: doubled rate, retention
+                    T.rate[j] = (j < ARA_PAIR_INTMAX ? 2.0 : 1.0) * L.rate[8 * c + j];
+                    T.ret[j] = (j < ARA_PAIR_INTMAX ? 2.0 : 1.0) * L.ret[8 * c + j];
+                    T.lim2[j] = 2.0 * L.lim[8 * c + j];
+                }
+                T.occ_ret2 = 2.0 * L.occ_ret;
+                T.occ_lim4 = 4.0 * L.occ_lim;
+                T.agg_ret4 = 4.0 * L.agg_ret;
+                T.agg_lim8 = 8.0 * L.agg_lim;
+                my_rows = rows + (size_t)layer * W + 8 * c;
+                ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
+                if (X) {
+                    mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
+                    inc_row = X == 2 && s.event_inc ? s.event_inc + (size_t)layer * s.event_inc_ld
+                                                    : nullptr;
+                }
+                cur_layer = layer;
+            }
+            const uint64_t beg = s.offsets[t] - base;
+            const uint64_t k = s.offsets[t + 1] - base - beg;
+            const uint32_t *ev = s.ids + beg;
+            const uint32_t *const ev_end = ev + k;
+            TrialState st{0.0, 0.0, 0.0, 0.0};
+            double xB = 0.0, own = 0.0;
+            uint32_t cur = zb;  // index of the last step's row (pipeline fill: zero rows)
+            // F4 increments: lane G - 1 at the step whose pair-0 event sits at YET position pos0
+            // finishes the event at pos0 - (P - 1); the first P - 1 steps finish no event
+            const uint64_t first_pos = beg + (P - 1);
+            auto out = [&](double inc8, uint64_t pos0) {
+                if constexpr (X == 2)
+                    if (inc_row && writer && pos0 >= first_pos) inc_row[pos0 - (P - 1)] = inc8 * 0.125;
+            };
+            auto single = [&](uint32_t idx0, uint64_t pos0) {
+                const uint32_t idx = next_index<P>(idx0, cur, c, gmask);
+                cur = idx;
+                Chunk<double> r[2];
+                gather2(my_rows, row_stride, idx, r);
+                out(pair_step<P>(r, T, c, gmask, xB, own, st), pos0);
+            };
+            // head: single events until the id pointer is 32-byte aligned
+            while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
+                single(row_index<MM>(look, load_id(ev), bad), (uint64_t)(ev - s.ids));
+                ++ev;
+            }
+            // body: chunks of 8 events; the ids of chunk i + 1 are in flight during chunk i, the
+            // gather of step j + 1 while step j is computed
+            const uint64_t n_chunks = (uint64_t)(ev_end - ev) / 8;
+            if (n_chunks) {
+                uint32_t id_c[8], id_n[8];
+                load_ids8(ev, id_c);
+                if (n_chunks > 1) load_ids8(ev + 8, id_n);
+                uint32_t ia = next_index<P>(row_index<MM>(look, id_c[0], bad), cur, c, gmask);
+                Chunk<double> ra[2], rb[2];
+                gather2(my_rows, row_stride, ia, ra);
+                uint64_t pos = (uint64_t)(ev - s.ids);
+#pragma unroll 1
+                for (uint64_t i = 0; i < n_chunks; ++i) {
+                    const bool more = i + 1 < n_chunks;
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        const uint32_t ib = next_index<P>(row_index<MM>(look, id_c[j + 1], bad), ia, c, gmask);
+                        gather2(my_rows, row_stride, pin(ib, own), rb);
+                        out(pair_step<P>(ra, T, c, gmask, xB, own, st), pos + j);
+                        const uint32_t id2 = j + 2 < 8 ? id_c[j + 2 < 8 ? j + 2 : 0] : id_n[0];
+                        const bool ok2 = j + 2 < 8 || more;
+                        const uint32_t ic =
+                            next_index<P>(ok2 ? row_index<MM>(look, id2, bad) : zb, ib, c, gmask);
+                        gather2(my_rows, row_stride, pin(ic, own), ra);
+                        out(pair_step<P>(rb, T, c, gmask, xB, own, st), pos + j + 1);
+                        cur = ib;
+                        ia = ic;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
+                    if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
+                    pos += 8;
+                }
+                ev += 8 * n_chunks;
+            }
+            // tail: remaining events one by one, then the P - 1 drain steps (pair 0 idle)
+            while (ev < ev_end) {
+                single(row_index<MM>(look, load_id(ev), bad), (uint64_t)(ev - s.ids));
+                ++ev;
+            }
+#pragma unroll
+            for (int d = 0; d < P - 1; ++d) single(zb + d, (uint64_t)(ev_end - s.ids) + d);
+            if (writer) {
+                ylt_row[t] = st.lr8 * 0.125;  // A8 (exact rescale)
+                if (X && mo_row) mo_row[t] = st.max4 * 0.25;
+            }
+        }
+        __syncwarp();
+        uint64_t b = 0;
+        if (lane == 0) b = warps + atomicAdd(s.counter, 1ull);
+        ticket = __shfl_sync(kFull, b, 0) * B + gw;
+    }
+    if (bad) atomicOr(s.err, kErrRange);
+    __syncthreads();  // the last block to finish resets the ticket counter for the next launch
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(s.done, 1u) == gridDim.x - 1) {
+            *s.counter = 0;
+            *s.done = 0;
+            __threadfence();
+        }
+    }
+}
+
+template <int P, int MINB, int MM, int X>
+__global__ void __launch_bounds__(kScanThreads, MINB)
+    pair_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
+                     const uint32_t *__restrict__ bitmap, const double *__restrict__ rows,
+                     const LayerTermsT<double> *__restrict__ terms, uint32_t n_layers)
+{
+    if constexpr (MM == 2) {
+        if (!probe_use_bitmap(s.probe)) {
+            pair_body<P, 1, X>(s, map, bitmap, rows, terms, n_layers);
+            return;
+        }
+    }
+    pair_body<P, MM, X>(s, map, bitmap, rows, terms, n_layers);
+}
+
+// Resident blocks per SM of one instantiation, cached per device (the dynamic shared memory
+// attribute is per device: set it before every first launch on a device).
+constexpr int kMaxDevices = 64;
+
+template <int P, int MINB, int MM, int X>
+cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                        cudaStream_t stream)
+{
+    auto kern = pair_scan_kernel<P, MINB, MM, X>;
+    const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
+    static std::atomic<int> occ_cache[kMaxDevices];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    int occ = (dev >= 0 && dev < kMaxDevices) ? occ_cache[dev].load() : 0;
+    if (occ == 0) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScanThreads, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        if (dev >= 0 && dev < kMaxDevices) occ_cache[dev].store(occ);
+    }
+    // One wave of resident blocks; the warp-batched tickets balance the work.  Fewer blocks when
+    // the tickets cannot fill them.
+    constexpr uint64_t groups_per_block = kScanThreads / (2 * P);
+    const uint64_t n_tickets = s.n_trials * st.n_layers;
+    uint64_t blocks = (uint64_t)sm_count * occ;
+    const uint64_t need = (n_tickets + groups_per_block - 1) / groups_per_block;
+    if (need < blocks) blocks = need;
+    if (blocks == 0) blocks = 1;
+    ScanLaunch sl = s;
+    sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
+    sl.bitmap_log2 = kBitmapLog2Scan;
+    kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
+        sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),
+        (const LayerTermsT<double> *)st.d_terms, st.n_layers);
+    return cudaGetLastError();
+}
+
+template <int P, int MINB, int X>
+cudaError_t launch_pair_mm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                           cudaStream_t stream)
+{
+    if (!st.d_rows_direct) return launch_pair<P, MINB, 0, X>(st, s, sm_count, stream);
+    if (st.map_mode == 1 || (X && st.map_mode == 2))
+        return launch_pair<P, MINB, 1, X>(st, s, sm_count, stream);
+    if constexpr (X == 0)
+        if (st.map_mode == 2) return launch_pair<P, MINB, 2, 0>(st, s, sm_count, stream);
+    return launch_pair<P, MINB, 0, X>(st, s, sm_count, stream);
+}
+
+template <int P, int MINB>
+cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                          cudaStream_t stream)
+{
+    if (s.event_inc) return launch_pair_mm<P, MINB, 2>(st, s, sm_count, stream);
+    if (s.max_occ) return launch_pair_mm<P, MINB, 1>(st, s, sm_count, stream);
+    return launch_pair_mm<P, MINB, 0>(st, s, sm_count, stream);
+}
+
+}  // namespace
+
+bool pair_scan_eligible(const DeviceStore &st, const ScanLaunch &s)
+{
+    // W = 32 / 64 (P > 1) serialise consecutive steps through the skewed chain: measured 1.5-1.7x
+    // slower than scan.cu's unskewed G = 4 kernel (profiles/r2_tune_pair.jsonl); tuning only
+    const bool wide_ok = st.pair_scan_wide && (st.width == 32 || st.width == 64);
+    return st.bits == 64 && st.scaled && s.counter && s.done && st.pair_scan &&
+           (st.width == 16 || wide_ok);
+}
+
+cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
+                             cudaStream_t stream, uint64_t *launches)
+{
+    if (s.n_trials == 0) return cudaSuccess;
+    ++*launches;
+    switch (st.width) {
+        case 16:
+            if (st.min_blocks == 4) return launch_pair_x<1, 4>(st, s, sm_count, stream);
+            return launch_pair_x<1, 3>(st, s, sm_count, stream);
+        case 32: return launch_pair_x<2, 3>(st, s, sm_count, stream);
+        case 64: return launch_pair_x<4, 3>(st, s, sm_count, stream);
+        default: --*launches; return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace ara

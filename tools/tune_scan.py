@@ -23,7 +23,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="headline")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--variants", default="2:0,4:0,1:0")
+    ap.add_argument("--variants", default="2:0,4:0,1:0",
+                    help="comma list of G:MINB[:MAPMODE], or name@KEY=VAL;KEY=VAL (env only)")
     ap.add_argument("--flags", type=int, default=0, help="ara_run flags (4 = ARA_RUN_BALANCE)")
     ap.add_argument("--sched", default="", help="ARA_SCAN_SCHED: static | dynamic")
     ap.add_argument("--precision", type=int, default=64)
@@ -47,11 +48,17 @@ def main():
     bytes_alg = n_ev * (4 + args.precision // 8 * E * L) + 8 * n * L + 8 * (n + 1)
     ref = None
     for v in args.variants.split(","):
-        g, mb, *mm = v.split(":")  # G:MINB[:ARA_MAP_MODE]
-        os.environ["ARA_SCAN_GROUP"] = g
-        os.environ["ARA_SCAN_MINB"] = mb
-        if mm:
-            os.environ["ARA_MAP_MODE"] = mm[0]
+        if "@" in v:  # name@KEY=VAL;KEY=VAL: tuning environment only
+            for kv in v.split("@", 1)[1].split(";"):
+                if kv:
+                    k, val = kv.split("=", 1)
+                    os.environ[k] = val
+        else:
+            g, mb, *mm = v.split(":")  # G:MINB[:ARA_MAP_MODE]
+            os.environ["ARA_SCAN_GROUP"] = g
+            os.environ["ARA_SCAN_MINB"] = mb
+            if mm:
+                os.environ["ARA_MAP_MODE"] = mm[0]
         os.environ["ARA_SCAN_SCHED"] = args.sched
         ctx = ara.Context(0, stream)
         ctx.ara_set_precision(args.precision)
