@@ -8,14 +8,20 @@ A step is one pass of the whole hot path over one batch: 
 scans its contiguous trial slice of the YET (ara_run: A2-A8, device-resident inputs), the YLT
 slices are all-gathered over NCCL (N > 1), and PML/TVaR at the return periods are computed
 (ara_metrics: A9).  The ELT store build (A1, ara_set_layers) is setup and not timed (it is the
-paper's preprocessing stage).  Weak scaling by default (trials are independent
-units): every rank scans its own 1M-trial slice of an N x 1M-trial YET, and
-PML/TVaR are taken over the whole gathered YLT; ``--scaling strong`` splits the 1M trials instead.  Inputs are synthetic (datagen/, seed 1308) with the paper's workload shape.
+paper's preprocessing stage).  Strong scaling by default: the configured workload
+(1M trials at the headline) is split over the ranks, as the paper decomposed one fixed workload
+over its GPUs; ``--scaling weak`` gives every rank the whole workload's
+trial count instead.  Inputs are synthetic (datagen/, seed 1308) with the paper's workload shape.
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA events on
 the context stream, max over ranks.  The YET (4 GB at the headline) is larger than L2, so every
-step streams it from HBM; the ELT store is L2-resident by design.  `e2e` repeats the step through
+step streams it from HBM; the ELT rows are L2-resident by design.  `e2e` repeats the step through
 the host-buffer C-ABI call (ara_run_host: pinned host YET copied in every step, YLT copied back).
+
+Parity (rank 0, after timing): the CPU oracle (oracle/, test infrastructure) runs Algorithm 1
+over every trial of the workload on the host cores; the YLT of the LAST timed step is compared
+with it entry by entry, and the step's PML/TVaR with the oracle's metrics of the oracle YLT
+(``parity`` in the JSON line).  The same oracle run is the ``cpu_baseline`` (N = 1).
 """
 from __future__ import annotations
 
@@ -72,6 +78,184 @@ def measured_peak():
             return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def gather_ceiling():
+    """Best measured rate of random 128-byte row gathers from L2 on this B200 (the scan's binding
+    resource: rows are L2 hits, DRAM carries only the id stream).  From the committed
+    microbenchmark (tools/microbench_rowpattern.cu): the fastest layout at any occupancy."""
+    import glob
+    best, src = None, None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*microbench_rowpattern*.jsonl"))):
+        for line in open(path):
+            d = json.loads(line)
+            if "events_per_s" in d and (best is None or d["events_per_s"] > best):
+                best, src = d["events_per_s"], f"{os.path.relpath(path, ROOT)}: {d['kernel']} " \
+                                                 f"at grid {d['grid']}"
+    return best, src
+
+
+def lib_sha16():
+    import hashlib
+    from paper_1308_2572_b200 import ara
+    with open(ara.LIB_PATH, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def ncu_entry(kernel: str, config: str):
+    """The committed ncu counters (profiles/scan_traffic.json) of THIS kernel instantiation in
+    THIS libara.so build and config, else None (stale counters are never reported)."""
+    path = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    try:
+        j = json.load(open(path))
+    except Exception:
+        return None
+    e = j.get(f"{kernel}|{lib_sha16()}|{config}")
+    return e if isinstance(e, dict) else None
+
+
+def roofline(args, spec, ctx, info, n_ev: int, n_loc: int, scan_ms: float) -> dict:
+    """Roofline of the dominant kernel (the scan), per launch on this rank.
+
+    Binding resource: random row gathers from L2 -- every trial-event
+    gathers its rows (gather_row_bytes) from the L2-resident store; `achieved` is those bytes over
+    the kernel time and `peak` the best measured 128-byte row-gather rate.  The north-star HBM
+    accounting (ids + E-wide rows + YLT + offsets against the copy bandwidth) is kept as the
+    secondary `north_star` view: its fraction exceeds 1 because the rows are L2 hits."""
+    L, E = spec.n_layers, spec.elts_per_layer
+    vb = args.precision // 8
+    t = scan_ms * 1e-3
+    peak_hbm, peak_src = measured_peak()
+    alg = n_ev * (4 + vb * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
+    ns = {"bound": "hbm", "unit": "GB/s", "bytes_alg_per_launch": alg,
+          "achieved": alg / t / 1e9, "peak": peak_hbm, "peak_source": peak_src,
+          "frac": alg / t / 1e9 / peak_hbm,
+          "bytes_model": f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide "
+                         "row segment per event, YLT, offsets (north-star accounting; > 1 "
+                         "because the rows are L2 hits, not HBM reads)"}
+    kern = info.last_kernel.decode()
+    ent = ncu_entry(kern, spec.name + ("+hoist" if args.hoist else ""))
+    traffic = ent["dram_bytes_per_launch"] if ent and ent.get("n_trials") == n_loc else None
+    physical = None
+    if ent:
+        physical = {k: ent[k] for k in ("dram_bytes_per_launch", "l2_to_l1_bytes", "l2_hit_rate",
+                                        "l1_data_pipe_busy", "l1_to_l2_request_busy",
+                                        "lts_throughput", "fp64_pipe", "alu_pipe",
+                                        "issue_active", "warps_per_sm", "bound") if k in ent}
+        physical["source"] = "profiles/scan_traffic.json (ncu --set full of this kernel " \
+                             "instantiation in this libara.so build)"
+    if args.hoist:
+        # the hoisted pass: one L1/L2 read of the per-event table per (occurrence, layer)
+        U = ctx.ara_layer_store_shape(0)[0]
+        hb = n_ev * (4 + vb * L) + U * L * (vb * E + vb) + 8 * n_loc * L + 8 * (n_loc + 1)
+        return {"bound": "hbm", "unit": "GB/s", "achieved": hb / t / 1e9, "peak": peak_hbm,
+                "frac": hb / t / 1e9 / peak_hbm, "traffic": traffic, "kernel": kern,
+                "kernel_ms": scan_ms, "bytes_alg_per_launch": hb, "peak_source": peak_src,
+                "bytes_model": f"n*k*(4 + {vb}*L) + U*L*({vb}*E + {vb}) + 8*n*L + 8*(n+1): "
+                               "hoisted-scan accounting (ids, one per-event layer loss per "
+                               "occurrence and layer, the table build, YLT, offsets)",
+                "physical": physical, "north_star_frac": None}
+    ceil_ev, ceil_src = gather_ceiling()
+    row_b = info.gather_row_bytes
+    gathered = n_ev * row_b
+    peak = ceil_ev * 128 / 1e9 if ceil_ev else None
+    achieved = gathered / t / 1e9
+    alu = None
+    if args.precision == 64:
+        ops = (5 * E + 9) * n_ev * L
+        alu_peak = 148 * 64 * 1.965e9
+        alu = {"unit": "fp64 lane-ops/s", "ops_per_trial_event": 5 * E + 9,
+               "achieved": ops / t, "peak": alu_peak, "frac": ops / t / alu_peak,
+               "peak_source": "148 SMs x 64 fp64 lanes/clk x 1965 MHz (nominal)"}
+    return {"bound": "l2_gather", "unit": "GB/s", "achieved": achieved, "peak": peak,
+            "frac": achieved / peak if peak else None, "traffic": traffic,
+            "kernel": kern, "kernel_ms": scan_ms,
+            "bytes_gathered_per_launch": gathered,
+            "bytes_model": f"n*k*{row_b}: every trial-event gathers its {row_b}-byte row "
+                           "segment(s) from the L2-resident store",
+            "peak_source": f"{ceil_src} ({ceil_ev:.3e} random 128-byte row gathers/s from "
+                           "L2; tools/microbench_rowpattern.cu)" if ceil_ev else None,
+            "north_star_frac": ns["frac"], "north_star": ns, "alu": alu, "physical": physical}
+
+
+def l2_note(info, spec) -> str:
+    rows = {0: "dense event-major rows through the 8 MB catalogue map",
+            1: "rows indexed by catalogue id (a (C+1)-row direct store; only the layer's "
+               "events' rows are touched)",
+            2: "rows indexed by catalogue id behind a 64 KB shared-memory presence bitmap "
+               "(a (C+1)-row direct store; only present events' rows are touched)"}
+    return (f"inputs larger than L2: the YET ({spec.n_trials} x {spec.k_max} ids) is streamed "
+            f"from HBM every step; the scan reads {rows.get(info.row_addressing, '?')}; the "
+            f"touched rows ({info.gather_row_bytes} B per event) are L2-resident")
+
+
+def oracle_run(ds, off, ev, precision: int = 64):
+    """The oracle over the whole YET on every host core: (YLT, seconds, DAT-build seconds,
+    threads).  Its direct access tables are built inside the call (the paper's preprocessing,
+    PAPER.md L61); that cost is measured with a 1-trial run and reported separately."""
+    import oracle
+    threads = max(1, len(os.sched_getaffinity(0)))
+    off1 = np.ascontiguousarray(off[:2])
+    t0 = time.perf_counter()
+    oracle.run_analysis(ds, n_threads=threads, trial_offsets=off1 - off1[0],
+                        events=ev[int(off[0]):int(off[1])], precision=precision)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ylt = oracle.run_analysis(ds, n_threads=threads, trial_offsets=off, events=ev,
+                              precision=precision)
+    return ylt, time.perf_counter() - t0, t_build, threads
+
+
+def compare_parity(got, want, res, L: int, kernel: str) -> dict:
+    """Every YLT entry of the last timed step against the oracle (bit-identical is the design
+    target; the north star's bar is |g - o| <= 1e-9 |o| and o = 0 => g = 0), and that step's
+    PML/TVaR against oracle.metrics of the oracle YLT (PML exact, TVaR within 1e-9)."""
+    import oracle
+    g, o = got.ravel(), want.ravel()
+    nz = o != 0
+    rel = np.abs(g[nz] - o[nz]) / np.abs(o[nz])
+    rows = [want[l] for l in range(L)] + ([oracle.portfolio_row(want)] if L > 1 else [])
+    pml_rel, tvar_rel, pml_exact = 0.0, 0.0, True
+    for i, row in enumerate(rows):
+        opml, otvar = oracle.metrics(row, P)
+        gpml, gtvar = np.asarray(res[i][0]), np.asarray(res[i][1])
+        pml_exact &= bool(np.array_equal(gpml, opml))
+        pml_rel = max(pml_rel, float(np.max(np.abs(gpml - opml) / np.maximum(np.abs(opml), 1e-300))))
+        tvar_rel = max(tvar_rel, float(np.max(np.abs(gtvar - otvar) / np.maximum(np.abs(otvar), 1e-300))))
+    out = {"ylt_n": int(o.size), "ylt_mismatches": int(np.count_nonzero(g != o)),
+           "ylt_max_rel": float(rel.max()) if rel.size else 0.0,
+           "ylt_zero_flips": int(np.count_nonzero((o == 0) & (g != 0))),
+           "pml_exact": pml_exact, "pml_max_rel": pml_rel, "tvar_max_rel": tvar_rel,
+           "metric_rows": len(rows), "return_periods": list(RETURN_PERIODS), "tol_rel": 1e-9,
+           "step": "the last timed step (steady-state kernel: " + kernel + ")",
+           "oracle": "oracle/oracle.c over every trial of the workload (host threads)"}
+    out["pass"] = (out["ylt_max_rel"] <= 1e-9 and out["ylt_zero_flips"] == 0 and
+                   pml_rel <= 1e-9 and tvar_rel <= 1e-9)
+    return out
+
+
+def cpu_baseline_from(spec, ds, off, t_or, t_build, threads, per_core=True):
+    """cpu_baseline from the parity oracle run (the whole workload on every host core) plus the
+    per-core rate of a ~2 s one-thread slice."""
+    import oracle
+    n_ev = int(off[-1] - off[0])
+    work = max(t_or - t_build, 1e-9)
+    value = n_ev * spec.n_layers / work
+    per_core_value = None
+    if per_core:
+        k = (spec.k_min + spec.k_max) // 2
+        n1 = max(1, min(spec.n_trials, int(2.0 * value / threads / max(1, k * spec.n_layers))))
+        o1, e1 = datagen.generate_yet(spec, ds.pool, 0, n1)
+        t0 = time.perf_counter()
+        oracle.run_analysis(ds, n_threads=1, trial_offsets=o1, events=e1)
+        t1 = time.perf_counter() - t0
+        per_core_value = int(o1[-1]) * spec.n_layers / max(t1 - t_build, 1e-9)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "per_core_value": per_core_value,
+            "sample": f"all {len(off) - 1} trials of the {spec.name} workload ({n_ev * spec.n_layers} "
+                      f"trial-events); oracle/oracle.c with {threads} threads: {t_or:.1f} s, minus "
+                      f"{t_build:.2f} s of direct-access-table build (preprocessing); the same run "
+                      "is the parity reference"}
 
 
 class ClockSampler:
@@ -243,7 +427,7 @@ def run_reference(args, spec):
     cb["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_name(spec),
                                             "parallelism": "host threads (oracle)"},
             "cpu_baseline": cb,
@@ -262,8 +446,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: the graded fp64 path; 32: the paper's float variant (F3)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: n_trials per rank (N x n in total); strong: n_trials split over ranks")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong: the workload's n_trials split over the ranks (default; the "
+                         "paper's decomposition); weak: n_trials per rank (N x n in total)")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-size oracle comparison of the last timed step")
     ap.add_argument("--hoist", action="store_true",
                     help="ARA_RUN_HOIST: Alg. 1 lines 4-17 once per distinct event per run, then "
                          "one table read per occurrence (SURVEY.md 7 deferred exact lever; "
@@ -390,6 +577,10 @@ def main():
             dist.barrier()
     ctx.ara_synchronize()
     launches = ctx.kernel_launches - launches0
+    # the last timed step's YLT (gathered over the ranks), for the parity check below
+    if world > 1 and args.metrics == "sharded" and not args.no_parity:  # not gathered in steps
+        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L])
+    last_ylt = (d_full_buf if world > 1 else d_ylt_buf)[:L].cpu().numpy() if rank == 0 else None
     ms = e0.elapsed_time(e1) / args.steps
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in scan_ev)
     if world > 1:
@@ -401,57 +592,10 @@ def main():
         n_ev_all = int(adist.sum_over_ranks([float(n_ev)])[0])
     trial_events = n_ev_all * spec.n_layers
     value = trial_events / (ms * 1e-3)
-    # roofline of the dominant kernel (the scan): algorithmic bytes per launch (DESIGN.md
-    # "Roofline"): per layer n*k*(4 + 8E) + n*8 (YLT) + (n+1)*8 (offsets); per rank.
+    info = ctx.ara_get_info()
+    last_kernel = info.last_kernel.decode()
     E = spec.elts_per_layer
-    # one fused launch covers all layers: the id stream and offsets are read once, every layer's
-    # E-wide fp64 row segment is gathered per event, every layer's YLT entry is written
-    vb = args.precision // 8  # bytes per stored loss
-    bytes_alg = n_ev * (4 + vb * E * L) + 8 * n_loc * L + 8 * (n_loc + 1)
-    bytes_model = (f"n*k*(4 + {vb}*E*L) + 8*n*L + 8*(n+1): ids once, each layer's E-wide row "
-                   "segment per event, YLT, offsets (north-star accounting)")
-    if args.hoist:  # what the hoisted pass moves: ids, one value per (occurrence, layer), the
-        # per-event table build (U rows of L*E losses read, U*L values written), YLT, offsets
-        U = ctx.ara_layer_store_shape(0)[0]
-        bytes_alg = (n_ev * (4 + vb * L) + U * L * (vb * E + vb) + 8 * n_loc * L
-                     + 8 * (n_loc + 1))
-        bytes_model = (f"n*k*(4 + {vb}*L) + U*L*({vb}*E + {vb}) + 8*n*L + 8*(n+1): ids, one "
-                       "per-event layer loss per (occurrence, layer), the per-event table build, "
-                       "YLT, offsets (hoisted-scan accounting; not comparable with the "
-                       "north-star bytes of the full scan)")
-    peak, peak_src = measured_peak()
-    achieved = bytes_alg / (scan_ms * 1e-3) / 1e9
-    traffic = None
-    physical = None
-    prof = os.path.join(ROOT, "profiles", "scan_traffic.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof)).get(spec.name + ("+hoist" if args.hoist else ""))
-            if pj and pj.get("n_trials") == n_loc and args.precision == 64:
-                traffic = pj["dram_bytes_per_launch"]
-                physical = {k: pj[k] for k in ("bound", "dram_bytes_per_launch", "l2_hit_rate",
-                                                "l1_data_pipe_busy", "lts_throughput",
-                                                "fp64_pipe", "alu_pipe", "issue_active")
-                            if k in pj}
-                physical["source"] = ("ncu capture committed in profiles/ (same kernel and "
-                                      "config; scan_traffic.json)")
-        except Exception:
-            pass
-
-    # Secondary (arithmetic) roofline of the full fp64 scan: the algorithmic fp64 operations per
-    # trial-event -- per (event, ELT) multiply, subtract, max, min and the ELT-sum add (5E), then
-    # occurrence terms (3), running sum (1), aggregate terms (3), difference (1), trial sum (1)
-    # -- against the fp64 lane-op peak: 148 SMs x 64 fp64 lanes per clock (ncu
-    # sm__sass_thread_inst_executed_op_dfma_pred_on peak_sustained) x the SM clock.  sm_100a has no
-    # fp64 min/max instruction, so the kernel issues each max/min as a DSETP (fp64 pipe) + 2 FSEL.
-    alu = None
-    if args.precision == 64 and not args.hoist:
-        ops = (5 * E + 9) * n_ev * L
-        alu_peak = 148 * 64 * 1.965e9
-        alu = {"unit": "fp64 lane-ops/s", "ops_per_trial_event": 5 * E + 9,
-               "achieved": ops / (scan_ms * 1e-3), "peak": alu_peak,
-               "frac": ops / (scan_ms * 1e-3) / alu_peak,
-               "peak_source": "148 SMs x 64 fp64 lanes/clk (ncu peak_sustained) x 1965 MHz"}
+    rf = roofline(args, spec, ctx, info, n_ev, n_loc, scan_ms)
 
     # ---- end to end through the host-buffer C-ABI call
     e2e = None
@@ -493,9 +637,21 @@ def main():
                        "the scan, YLT back to host) + YLT upload + ara_metrics; wall clock, "
                        "median of steps, max over ranks"}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_measure(spec, ds)
+    # ---- parity of the last timed step (its YLT is still in the buffers) against the oracle run
+    # over every trial of the workload; the same run is the CPU baseline (rank 0)
+    parity, cpu = None, None
+    if rank == 0 and not (args.no_parity and (args.no_cpu_baseline or world > 1)):
+        got = last_ylt
+        if world > 1:  # rank 0 regenerates the whole YET (counter-based: identical trials)
+            off_all, ev_all = datagen.generate_yet(spec, ds.pool, 0, n_total)
+        else:
+            off_all, ev_all = h_off_np, h_ids.numpy().view(np.uint32)
+        want, t_or, t_build, threads = oracle_run(ds, off_all, ev_all, args.precision)
+        if not args.no_parity:
+            parity = compare_parity(got, want, res, L, last_kernel)
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline_from(spec, ds, off_all, t_or, t_build, threads,
+                                    per_core=True)
 
     if rank == 0:
         line = {
@@ -517,22 +673,10 @@ def main():
                                          "all-reduced per pass)" if args.metrics == "sharded"
                                          else "(NCCL all-gather of the YLT for PML/TVaR)")
                        if world > 1 else "1 GPU",
-                       "l2": "inputs larger than L2: the 4 GB YET is streamed from HBM every "
-                             "step; the ELT store (2.6 MB rows + 8 MB map) is L2-resident",
+                       "l2": l2_note(info, spec),
                        "return_periods": list(RETURN_PERIODS)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("hoisted_scan_kernel + hoist_oc_kernel (ara_run, ARA_RUN_HOIST)"
-                                    if args.hoist else
-                                    f"scan_kernel (ara_run; W = {ctx.ara_layer_store_shape(0)[1]})"),
-                         "kernel_ms": scan_ms,
-                         "bytes_alg_per_launch": bytes_alg, "peak_source": peak_src,
-                         "bytes_model": bytes_model,
-                         "physical": physical, "alu": alu,
-                         "note": ("frac > 1 because the north-star bytes count every gathered "
-                                  "row as an HBM read: the row store is L2-resident by design "
-                                  "(see traffic = DRAM bytes per launch from ncu, and physical)")
-                                 if achieved > peak else None},
+            "roofline": rf,
+            "parity": parity,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -546,6 +690,8 @@ def main():
         if args.json_out:
             with open(args.json_out, "w") as f:
                 f.write(s + "\n")
+    if world > 1:
+        dist.barrier()  # rank 0's oracle run may outlast the others' teardown
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

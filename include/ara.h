@@ -296,6 +296,20 @@ ara_status ara_metrics_sharded(ara_ctx *ctx, const double *d_ylt_slice, uint64_t
 ara_status ara_metrics_host(ara_ctx *ctx, const double *h_ylt_row, uint64_t n, uint32_t n_p,
                             const double *p, double *pml_out, double *tvar_out);
 
+/* F4 ("financial functions or filters are then applied on the
+ * aggregate loss values"; L32): the exceedance-probability curve of one row -- the AEP curve of a
+ * YLT row (annual aggregate loss per trial) or the OEP curve of a max_occ row of ara_run_outputs
+ * (annual maximum occurrence loss).  d_curve[i] = the (i+1)-th largest of d_row[0..n), i.e. the
+ * loss whose empirical exceedance probability is (i+1)/n (return period n/(i+1) years); -0 is
+ * returned as +0.  Every PML of ara_metrics is a point on it: PML(p) = d_curve[n - ceil(p n)]
+ * (readings R11, R15).
+ *   d_row    device, n doubles, caller-owned, read only;
+ *   d_curve  device, n doubles, caller-owned, must not overlap d_row.
+ * Stream-ordered on the context stream (no host synchronisation); the context keeps an internal
+ * scratch buffer (2n keys + the sort's temporary storage), grown on demand.
+ * Errors: ARA_ERR_EMPTY (n = 0), ARA_ERR_ARG (NULL or overlapping pointers), ARA_ERR_CUDA. */
+ara_status ara_ep_curve(ara_ctx *ctx, const double *d_row, uint64_t n, double *d_curve);
+
 /* Introspection (tests, benchmarks). */
 typedef struct {
     uint32_t catalogue_size;
@@ -314,6 +328,11 @@ typedef struct {
                                     per layer (one fused launch); 1 = union rows, layer sums
                                     through a shared-memory F row; 2 = union rows, layer sums
                                     through register shuffles.  Identical results.          */
+    uint32_t gather_row_bytes;   /* row bytes the scan gathers per event (all layers; the
+                                    union row when layer_kernel > 0)                        */
+    char last_kernel[64];        /* the scan-kernel instantiation the last ara_run* launched,
+                                    as ncu names it (e.g. "pair_scan_kernel<1, 3, 1, 0>");
+                                    "" before the first run                                 */
 } ara_info;
 
 ara_status ara_get_info(const ara_ctx *ctx, ara_info *out);

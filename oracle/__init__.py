@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_apply_occurrence_terms_f32.restype = f
         L.oracle_metrics.argtypes = [p, u64, u32, p, p, p]
         L.oracle_metrics.restype = ctypes.c_int
+        L.oracle_ep_curve.argtypes = [p, u64, p]
+        L.oracle_ep_curve.restype = ctypes.c_int
         L.oracle_portfolio_row.argtypes = [p, u32, u64, u64, p]
         L.oracle_portfolio_row.restype = None
         _lib = L
@@ -186,3 +188,14 @@ def metrics(ylt_row, p: Sequence[float]):
     if st:
         raise MemoryError("oracle: out of memory")
     return pml, tvar
+
+
+def ep_curve(row) -> np.ndarray:
+    """Exceedance-probability curve (F4, reading R15): the row sorted from the largest value
+    down; entry i has empirical exceedance probability (i+1)/n.  AEP from a YLT row, OEP from
+    the per-trial maximum occurrence losses."""
+    v = np.ascontiguousarray(row, dtype=np.float64)
+    out = np.empty(v.shape[0])
+    if lib().oracle_ep_curve(_ptr(v), v.shape[0], _ptr(out)) == -1:
+        raise ValueError("oracle: empty row")
+    return out

@@ -130,3 +130,20 @@ int oracle_metrics(const double *ylt_row, uint64_t n, uint32_t n_p, const double
     free(v);
     return 0;
 }
+
+/* Exceedance-probability curve of a YLT-like row ("financial
+ * functions or filters are then applied on the aggregate loss values"; reading R15 of DESIGN.md):
+ * the row sorted from the largest value down, out[i] = the (i+1)-th largest, whose empirical
+ * exceedance probability is (i+1)/n (return period n/(i+1) years).  From a YLT row it is the AEP
+ * curve, from the per-trial maximum occurrence losses (R13) the OEP curve.  The nearest-rank PML
+ * of R11 is a point on it: PML(p) = out[n - ceil(p n)].  Returns 0, -1 if n == 0, -3 out of
+ * memory. */
+static int o_cmp_desc(const void *a, const void *b) { return o_cmp(b, a); }
+
+int oracle_ep_curve(const double *row, uint64_t n, double *out)
+{
+    if (n == 0) return -1;
+    memcpy(out, row, n * sizeof(double));
+    qsort(out, n, sizeof(double), o_cmp_desc);
+    return 0;
+}

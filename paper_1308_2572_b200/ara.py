@@ -32,7 +32,7 @@ EXPORTS = ["ara_status_string", "ara_create", "ara_set_precision", "ara_set_stre
            "ara_load_elts", "ara_set_layers", "ara_run", "ara_run_outputs", "ara_run_host",
            "ara_synchronize",
            "ara_metrics", "ara_metrics_host", "ara_metrics_rows", "ara_metrics_sharded",
-           "ara_portfolio_ylt",
+           "ara_portfolio_ylt", "ara_ep_curve",
            "ara_get_info",
            "ara_layer_store_shape",
            "ara_export_store"]
@@ -75,7 +75,8 @@ class Info(ctypes.Structure):
                 ("n_layers", ctypes.c_uint32), ("max_row_width", ctypes.c_uint32),
                 ("store_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("device", ctypes.c_int), ("sm_count", ctypes.c_int),
-                ("row_addressing", ctypes.c_int), ("layer_kernel", ctypes.c_int)]
+                ("row_addressing", ctypes.c_int), ("layer_kernel", ctypes.c_int),
+                ("gather_row_bytes", ctypes.c_uint32), ("last_kernel", ctypes.c_char * 64)]
 
 
 def _load() -> ctypes.CDLL:
@@ -106,6 +107,7 @@ def _load() -> ctypes.CDLL:
         "ara_metrics": ([p, p, u64, u32, p, p, p], i32),
         "ara_metrics_host": ([p, p, u64, u32, p, p, p], i32),
         "ara_portfolio_ylt": ([p, p, u64, u64, p, u32], i32),
+        "ara_ep_curve": ([p, p, u64, p], i32),
         "ara_metrics_rows": ([p, p, u32, u64, u64, u32, p, p, p], i32),
         "ara_metrics_sharded": ([p, p, u64, u64, u32, p, p, p, p, u64, SHARD_REDUCE, p], i32),
         "ara_get_info": ([p, ctypes.POINTER(Info)], i32),
@@ -238,6 +240,15 @@ class Context:
             raise TypeError("h_ylt must be a contiguous float64 numpy array")
         self._check(lib().ara_run_host(self._ptr, to.shape[0] - 1, _hptr(to), _hptr(ev),
                                        _hptr(h_ylt), ylt_ld, flags))
+
+    def ara_ep_curve(self, d_row, d_curve):
+        """F4 exceedance curve: d_curve = d_row sorted from the largest value down (stream-
+        ordered; both 1-D float64 CUDA tensors of the same length)."""
+        n = d_row.numel()
+        if d_curve.numel() != n:
+            raise ValueError("d_curve must have d_row's length")
+        self._check(lib().ara_ep_curve(self._ptr, _dptr(d_row, "torch.float64"), n,
+                                       _dptr(d_curve, "torch.float64")))
 
     def ara_synchronize(self):
         self._check(lib().ara_synchronize(self._ptr))

@@ -29,6 +29,7 @@ struct ara_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;
     std::string err;
+    std::string last_kernel;  // ara_info.last_kernel
 
     bool have_elts = false;
     bool have_layers = false;
@@ -60,6 +61,7 @@ struct ara_ctx {
     uint32_t *h_err = nullptr;  // pinned mirror
     uint64_t launches = 0;
     ara::MetricsScratch metrics;
+    ara::EpScratch ep;
     ara::SortScratch sort;
 
     // ara_run_host staging (double-buffered)
@@ -260,7 +262,7 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     // ARA_SCAN_SCHED=static|dynamic selects the plain round-robin / per-group ticket schedules
     // (tuning); the F4 outputs of an fp32 store use per-group tickets.
     const bool balance = ctx->sched == 0 && (!extra || ctx->store.bits == 64) &&
-                         n <= 0xffffffffull;  // u32 permutation
+                         n <= 0x7fffffffull;  // u32 permutation, CUB's int item count
     const bool sorted = balance && !ctx->lengths_equal;
     const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
     const uint32_t *perm = nullptr;
@@ -329,6 +331,7 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                     : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
+    if (ara::t_last_kernel) ctx->last_kernel = ara::t_last_kernel;
     return ARA_OK;
 }
 
@@ -651,6 +654,7 @@ void ara_destroy(ara_ctx *ctx)
     cudaFreeHost(ctx->h_err);
     cudaFree(ctx->metrics.d_buf);
     cudaFree(ctx->metrics.d_shard);
+    cudaFree(ctx->ep.d_buf);
     cudaFree(ctx->sort.d_buf);
     for (int i = 0; i < 2; ++i) {
         cudaFree(ctx->d_ids_stage[i]);
@@ -854,13 +858,20 @@ ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_tr
         if (!o.max_occ_ld) o.max_occ_ld = n_trials;
         if (o.ylt_ld < n_trials || (o.max_occ && o.max_occ_ld < n_trials))
             return fail(ctx, ARA_ERR_ARG, "leading dimension < n_trials");
-        if (o.event_inc) {  // needs the YET's event count: two 8-byte reads of the offsets
-            uint64_t ends[2];
+        // the YET's event count (increments, validation): two 8-byte reads of the offsets
+        uint64_t ends[2] = {0, 0};
+        if (o.event_inc || (flags & ARA_RUN_VALIDATE)) {
             ARA_CUDA(ctx, cudaMemcpyAsync(&ends[0], d_trial_offsets, 8, cudaMemcpyDeviceToHost,
                                           ctx->stream));
             ARA_CUDA(ctx, cudaMemcpyAsync(&ends[1], d_trial_offsets + n_trials, 8,
                                           cudaMemcpyDeviceToHost, ctx->stream));
             ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            if (ends[1] < ends[0])
+                return fail(ctx, ARA_ERR_VALIDATION,
+                            "trial offsets decrease (offsets[n] = %llu < offsets[0] = %llu)",
+                            (unsigned long long)ends[1], (unsigned long long)ends[0]);
+        }
+        if (o.event_inc) {
             const uint64_t n_ev = ends[1] - ends[0];
             if (!o.event_inc_ld) o.event_inc_ld = n_ev;
             if (o.event_inc_ld < n_ev)
@@ -870,9 +881,9 @@ ara_status ara_run_outputs(ara_ctx *ctx, uint64_t n_trials, const uint64_t *d_tr
         if (flags & ARA_RUN_VALIDATE) {
             ara_status s = check_device_error(ctx);  // report earlier deferred errors first
             if (s != ARA_OK) return s;
-            cudaError_t e = ara::launch_validate(d_trial_offsets, d_event_ids, n_trials, ctx->C,
-                                                 ctx->d_err, ctx->sm_count, ctx->stream,
-                                                 &ctx->launches);
+            cudaError_t e = ara::launch_validate(d_trial_offsets, d_event_ids, n_trials,
+                                                 ends[1] - ends[0], ctx->C, ctx->d_err,
+                                                 ctx->sm_count, ctx->stream, &ctx->launches);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "validate kernel launch");
             s = check_device_error(ctx);
             if (s != ARA_OK) return s;
@@ -983,6 +994,12 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
                                               n_ev * 4, cudaMemcpyHostToDevice, ctx->copy_stream));
             ARA_CUDA(ctx, cudaEventRecord(ctx->ev_copy[buf], ctx->copy_stream));
             ARA_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_copy[buf], 0));
+            if (flags & ARA_RUN_VALIDATE) {  // ids of this chunk (the offsets were checked above)
+                cudaError_t e = ara::launch_validate(ctx->d_off_stage[buf], ctx->d_ids_stage[buf],
+                                                     t1 - t0, n_ev, ctx->C, ctx->d_err,
+                                                     ctx->sm_count, ctx->stream, &ctx->launches);
+                if (e != cudaSuccess) return cuda_fail(ctx, e, "validate kernel launch");
+            }
             s = launch_layers(ctx, t1 - t0, ctx->d_off_stage[buf], ctx->d_ids_stage[buf],
                               ctx->d_ylt_stage + t0, n_trials, flags);
             if (s != ARA_OK) return s;
@@ -991,10 +1008,28 @@ ara_status ara_run_host(ara_ctx *ctx, uint64_t n_trials, const uint64_t *h_trial
             buf ^= 1;
             t0 = t1;
         }
+        // device errors (ids out of range) are reported before anything reaches h_ylt
+        s = check_device_error(ctx);
+        if (s != ARA_OK) return s;
         ARA_CUDA(ctx, cudaMemcpy2DAsync(h_ylt, ld * 8, ctx->d_ylt_stage, n_trials * 8,
                                         n_trials * 8, n_layers, cudaMemcpyDeviceToHost,
                                         ctx->stream));
-        return check_device_error(ctx);
+        ARA_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return ARA_OK;
+    });
+}
+
+ara_status ara_ep_curve(ara_ctx *ctx, const double *d_row, uint64_t n, double *d_curve)
+{
+    return guarded(ctx, __func__, [&]() -> ara_status {
+        if (n == 0) return fail(ctx, ARA_ERR_EMPTY, "n is 0");
+        if (!d_row || !d_curve) return fail(ctx, ARA_ERR_ARG, "device pointer is NULL");
+        if (d_row < d_curve + n && d_curve < d_row + n)
+            return fail(ctx, ARA_ERR_ARG, "d_row and d_curve overlap");
+        cudaError_t e = ara::launch_ep_curve(d_row, n, d_curve, ctx->ep, ctx->sm_count,
+                                             ctx->stream, &ctx->launches);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "exceedance curve");
+        return ARA_OK;
     });
 }
 
@@ -1116,6 +1151,11 @@ ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
     out->row_addressing = ctx->have_layers ? ctx->store.map_mode : 0;
     out->layer_kernel = !ctx->have_layers || !ctx->store.uni.enabled ? 0
                         : 1 + (ctx->store.uni.shfl != 0);
+    out->gather_row_bytes = !ctx->have_layers ? 0
+                            : ctx->store.uni.enabled
+                                ? 8 * 8 * ctx->store.uni.GU
+                                : ctx->store.n_layers * ctx->store.width * (ctx->store.bits / 8);
+    snprintf(out->last_kernel, sizeof(out->last_kernel), "%s", ctx->last_kernel.c_str());
     return ARA_OK;
 }
 

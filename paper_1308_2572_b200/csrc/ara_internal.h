@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -218,7 +219,7 @@ cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint6
                              const uint32_t *d_map, uint32_t C, unsigned long long *probe,
                              cudaStream_t stream, uint64_t *launches);
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
-                            uint32_t catalogue_size, uint32_t *err, int sm_count,
+                            uint64_t n_ev, uint32_t catalogue_size, uint32_t *err, int sm_count,
                             cudaStream_t stream, uint64_t *launches);
 
 // metrics.cu
@@ -241,12 +242,57 @@ cudaError_t launch_metrics_sharded(const double *d_slice, uint64_t n_local, uint
                                    double *tvar_out, char *d_xbuf, ShardReduce reduce,
                                    void *user, MetricsScratch &scratch, int sm_count,
                                    cudaStream_t stream, uint64_t *launches);
+// F4 exceedance curve (ara_ep_curve): the row sorted descending, stream-ordered.
+struct EpScratch {
+    void *d_buf = nullptr;
+    size_t bytes = 0;
+};
+cudaError_t launch_ep_curve(const double *d_row, uint64_t n, double *d_out, EpScratch &sc,
+                            int sm_count, cudaStream_t stream, uint64_t *launches);
 // PML/TVaR of n_rows rows (row r at d_rows + r * ld, n entries each) in shared passes;
 // pml_out / tvar_out are [n_rows][n_p].
 cudaError_t launch_metrics(const double *d_rows, uint64_t ld, uint32_t n_rows, uint64_t n,
                            uint32_t n_p, const double *p, double *pml_out, double *tvar_out,
                            MetricsScratch &scratch, int sm_count, int device, cudaStream_t stream,
                            uint64_t *launches);
+
+// Name of the last scan-kernel instantiation launched by this host thread, as ncu prints it
+// (e.g. "pair_scan_kernel<1, 3, 1, 0>"); ara_run copies it into ara_info.last_kernel, and the
+// bench keys its committed ncu counters by it.  Set by the launchers.
+extern thread_local const char *t_last_kernel;
+inline std::string kernel_arg(int v) { return std::to_string(v); }
+inline std::string kernel_arg(bool v) { return v ? "1" : "0"; }
+inline std::string kernel_arg(const char *v) { return v; }
+template <typename... A>
+std::string kernel_name(const char *base, A... args)
+{
+    std::string s = std::string(base) + "<";
+    bool first = true;
+    ((s += (first ? "" : ", ") + kernel_arg(args), first = false), ...);
+    return s + ">";
+}
+
+// Resident blocks per SM of kernel `func` (`threads` threads, `smem` bytes of dynamic shared
+// memory) on the current device.  The dynamic shared memory attribute is per device, so it is
+// set on each device's first launch; `cache` is the launcher's per-instantiation static array.
+constexpr int kMaxDevices = 64;
+inline cudaError_t blocks_per_sm(const void *func, int threads, size_t smem,
+                                 std::atomic<int> (&cache)[kMaxDevices], int &occ)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const bool cached = dev >= 0 && dev < kMaxDevices;
+    occ = cached ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (occ > 0) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    if (cached) cache[dev].store(occ, std::memory_order_relaxed);
+    return cudaSuccess;
+}
 
 constexpr uint32_t kErrRange = 1u;
 constexpr uint32_t kErrOffsets = 2u;

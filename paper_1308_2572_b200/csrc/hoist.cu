@@ -250,17 +250,11 @@ cudaError_t launch_hs(const DeviceStore &st, const ScanLaunch &s, int sm_count,
 {
     constexpr int T = hoist_threads<LP>();
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Hoist) : 0;
-    static int occ = 0;
-    if (occ == 0) {
-        cudaError_t e = cudaFuncSetAttribute(hoisted_scan_kernel<LP, R, BAL, MM>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, hoisted_scan_kernel<LP, R, BAL, MM>, T, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
+    static std::atomic<int> occ_cache[kMaxDevices];  // resident blocks per SM, per device
+    int occ = 0;
+    cudaError_t oe = blocks_per_sm((const void *)hoisted_scan_kernel<LP, R, BAL, MM>, T, smem,
+                                   occ_cache, occ);
+    if (oe != cudaSuccess) return oe;
     // one lane per trial: a balanced single wave where possible
     const uint64_t max_blocks = (uint64_t)sm_count * occ;
     const uint64_t rounds = (s.n_trials + max_blocks * T - 1) / (max_blocks * T);
@@ -270,6 +264,9 @@ cudaError_t launch_hs(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     if (blocks > max_blocks) blocks = max_blocks;
     ScanLaunch sl = s;
     sl.bitmap_log2 = kBitmapLog2Hoist;
+    static const std::string name = kernel_name("hoisted_scan_kernel", LP,
+                                                sizeof(R) == 8 ? "double" : "float", BAL, MM);
+    t_last_kernel = name.c_str();
     hoisted_scan_kernel<LP, R, BAL, MM><<<(unsigned)blocks, T, smem, stream>>>(
         sl, st.d_map, st.d_oc_bitmap, (const R *)st.d_oc, (const LayerTermsT<R> *)st.d_terms,
         st.n_layers);

@@ -10,6 +10,8 @@
 #include <cooperative_groups.h>
 #include <string.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -595,6 +597,58 @@ cudaError_t launch_portfolio_row(const double *d_ylt, uint32_t n_layers, uint64_
     const uint64_t want = (n + 255) / 256;
     const unsigned blocks = (unsigned)std::min<uint64_t>(want, (uint64_t)sm_count * 8);
     portfolio_row_kernel<<<blocks, 256, 0, stream>>>(d_ylt, n_layers, n, ld, d_out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// F4: exceedance-probability curves (reading R15).  The row's order-preserving keys
+// (to_key: -0 canonicalised to +0) are sorted descending with CUB's radix sort (a library sort;
+// the keys and the decode are this file's kernels) and decoded back: out[i] = the (i+1)-th
+// largest value, exceedance probability (i+1)/n.
+namespace {
+__global__ void ep_keys_kernel(const double *__restrict__ v, uint64_t n, uint64_t *keys)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = to_key(v[i]);
+}
+
+__global__ void ep_decode_kernel(const uint64_t *__restrict__ keys, uint64_t n, double *out)
+{
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = from_key(keys[i]);
+}
+}  // namespace
+
+cudaError_t launch_ep_curve(const double *d_row, uint64_t n, double *d_out, EpScratch &sc,
+                            int sm_count, cudaStream_t stream, uint64_t *launches)
+{
+    if (n == 0) return cudaSuccess;
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortKeysDescending(
+        nullptr, temp, (const uint64_t *)nullptr, (uint64_t *)nullptr, (int64_t)n, 0, 64, stream);
+    if (e != cudaSuccess) return e;
+    const size_t need = 2 * n * sizeof(uint64_t) + temp + 256;
+    if (sc.bytes < need) {
+        cudaFree(sc.d_buf);  // synchronising: no earlier curve still uses the old buffer
+        sc.d_buf = nullptr;
+        sc.bytes = 0;
+        e = cudaMalloc(&sc.d_buf, need);
+        if (e != cudaSuccess) return e;
+        sc.bytes = need;
+    }
+    uint64_t *keys = (uint64_t *)sc.d_buf, *sorted = keys + n;
+    void *tmp = (void *)(((uintptr_t)(sorted + n) + 255) & ~(uintptr_t)255);
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count * 8);
+    *launches += 3;  // keys, the CUB sort (a few internal kernels counted once), decode
+    ep_keys_kernel<<<blocks, 256, 0, stream>>>(d_row, n, keys);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceRadixSort::SortKeysDescending(tmp, temp, keys, sorted, (int64_t)n, 0, 64,
+                                                 stream);
+    if (e != cudaSuccess) return e;
+    ep_decode_kernel<<<blocks, 256, 0, stream>>>(sorted, n, d_out);
     return cudaGetLastError();
 }
 

@@ -275,17 +275,11 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
                        const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Union) : 0;
-    static int occ = 0;
-    if (occ == 0) {
-        cudaError_t e = cudaFuncSetAttribute(portfolio_kernel<GU, BAL, MM, SH>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, portfolio_kernel<GU, BAL, MM, SH>,
-                                                          kScanThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
+    static std::atomic<int> occ_cache[kMaxDevices];  // resident blocks per SM, per device
+    int occ = 0;
+    cudaError_t oe = blocks_per_sm((const void *)portfolio_kernel<GU, BAL, MM, SH>,
+                                   kScanThreads, smem, occ_cache, occ);
+    if (oe != cudaSuccess) return oe;
     const uint64_t per_block = kScanThreads / GU;
     const uint64_t max_blocks = (uint64_t)sm_count * occ;
     const uint64_t rounds = (s.n_trials + max_blocks * per_block - 1) / (max_blocks * per_block);
@@ -296,6 +290,8 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
     ScanLaunch sl = s;
     sl.zero_base = MM ? us.zero_base_direct : us.zero_base;
     sl.bitmap_log2 = kBitmapLog2Union;
+    static const std::string name = kernel_name("portfolio_kernel", GU, BAL, MM, SH);
+    t_last_kernel = name.c_str();
     portfolio_kernel<GU, BAL, MM, SH><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();

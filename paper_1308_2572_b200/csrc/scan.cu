@@ -39,6 +39,9 @@
 #endif
 
 namespace ara {
+
+thread_local const char *t_last_kernel = nullptr;
+
 namespace {
 
 using namespace scan_detail;
@@ -410,21 +413,18 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     scan_body<G, CH, X, R, BAL, MM, D>(s, map, bitmap, rows, terms, n_layers);
 }
 
-// Device-side validation (ARA_RUN_VALIDATE): offsets non-decreasing, ids in [1, C].
+// Device-side validation (ARA_RUN_VALIDATE): offsets non-decreasing, ids in [1, C].  n_ev =
+// offsets[n] - offsets[0] comes from the host, which has checked offsets[n] >= offsets[0]: the
+// id pass never reads past the YET whatever the interior offsets hold.
 __global__ void validate_kernel(const uint64_t *__restrict__ offsets,
                                 const uint32_t *__restrict__ ids, uint64_t n_trials,
-                                uint32_t C, uint32_t *err)
+                                uint64_t n_ev, uint32_t C, uint32_t *err)
 {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t e = 0;
     for (uint64_t t = tid; t < n_trials; t += stride)
         if (offsets[t + 1] < offsets[t]) e |= kErrOffsets;
-    if (__syncthreads_or(e != 0)) {
-        if (threadIdx.x == 0) atomicOr(err, kErrOffsets);
-        return;
-    }
-    const uint64_t n_ev = offsets[n_trials] - offsets[0];
     for (uint64_t i = tid; i < n_ev; i += stride)
         if (ids[i] - 1u >= C) e |= kErrRange;
     if (e) atomicOr(err, e);
@@ -478,17 +478,11 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                        cudaStream_t stream)
 {
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
-    static int occ = 0;  // resident blocks per SM for this instantiation
-    if (occ == 0) {
-        cudaError_t e = cudaFuncSetAttribute(scan_kernel<G, CH, MINB, X, R, BAL, MM, D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &occ, scan_kernel<G, CH, MINB, X, R, BAL, MM, D>, kScanThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
+    static std::atomic<int> occ_cache[kMaxDevices];  // resident blocks per SM, per device
+    int occ = 0;
+    cudaError_t oe = blocks_per_sm((const void *)scan_kernel<G, CH, MINB, X, R, BAL, MM, D>,
+                                   kScanThreads, smem, occ_cache, occ);
+    if (oe != cudaSuccess) return oe;
     // Balanced single wave over (trial, layer) groups: every trial slot gets ceil(n / slots)
     // or one fewer trials; the number of groups is a multiple of L (a lane keeps its layer) and,
     // where possible, the grid is a multiple of the SM count.
@@ -511,6 +505,9 @@ cudaError_t launch_gcm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
+    static const std::string name = kernel_name("scan_kernel", G, CH, MINB, X,
+                                                sizeof(R) == 8 ? "double" : "float", BAL, MM, D);
+    t_last_kernel = name.c_str();
     scan_kernel<G, CH, MINB, X, R, BAL, MM, D><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const R *)(MM ? st.d_rows_direct : st.d_rows),
         (const LayerTermsT<R> *)st.d_terms, st.n_layers);
@@ -719,7 +716,7 @@ cudaError_t launch_length_check(const uint64_t *offsets, uint64_t n, SortScratch
                                 uint64_t *launches)
 {
     if (n == 0) return cudaSuccess;
-    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    if (n > 0x7fffffffull) return cudaErrorInvalidValue;  // CUB's int item count
     size_t temp;
     cudaError_t e = sort_scratch(n, sc, temp, stream);
     if (e != cudaSuccess) return e;
@@ -734,7 +731,7 @@ cudaError_t launch_length_sort(const uint64_t *offsets, uint64_t n, SortScratch 
                                cudaStream_t stream, uint64_t *launches, unsigned long long *differ)
 {
     if (n == 0) return cudaSuccess;
-    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    if (n > 0x7fffffffull) return cudaErrorInvalidValue;  // CUB's int item count
     size_t temp;
     cudaError_t e = sort_scratch(n, sc, temp, stream);
     if (e != cudaSuccess) return e;
@@ -764,13 +761,13 @@ cudaError_t launch_hit_probe(const uint64_t *offsets, const uint32_t *ids, uint6
 }
 
 cudaError_t launch_validate(const uint64_t *offsets, const uint32_t *ids, uint64_t n_trials,
-                            uint32_t catalogue_size, uint32_t *err, int sm_count,
+                            uint64_t n_ev, uint32_t catalogue_size, uint32_t *err, int sm_count,
                             cudaStream_t stream, uint64_t *launches)
 {
     if (n_trials == 0) return cudaSuccess;
     ++*launches;
-    validate_kernel<<<sm_count * 8, 256, 0, stream>>>(offsets, ids, n_trials, catalogue_size,
-                                                     err);
+    validate_kernel<<<sm_count * 8, 256, 0, stream>>>(offsets, ids, n_trials, n_ev,
+                                                     catalogue_size, err);
     return cudaGetLastError();
 }
 

@@ -37,8 +37,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <atomic>
-
 #include "ara_internal.h"
 #include "scan_common.cuh"
 
@@ -312,10 +310,6 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
     pair_body<P, MM, X>(s, map, bitmap, rows, terms, n_layers);
 }
 
-// Resident blocks per SM of one instantiation, cached per device (the dynamic shared memory
-// attribute is per device: set it before every first launch on a device).
-constexpr int kMaxDevices = 64;
-
 template <int P, int MINB, int MM, int X>
 cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream)
@@ -323,18 +317,9 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     auto kern = pair_scan_kernel<P, MINB, MM, X>;
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
     static std::atomic<int> occ_cache[kMaxDevices];
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    int occ = 0;
+    cudaError_t e = blocks_per_sm((const void *)kern, kScanThreads, smem, occ_cache, occ);
     if (e != cudaSuccess) return e;
-    int occ = (dev >= 0 && dev < kMaxDevices) ? occ_cache[dev].load() : 0;
-    if (occ == 0) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kScanThreads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        if (dev >= 0 && dev < kMaxDevices) occ_cache[dev].store(occ);
-    }
     // One wave of resident blocks; the warp-batched tickets balance the work.  Fewer blocks when
     // the tickets cannot fill them.
     constexpr uint64_t groups_per_block = kScanThreads / (2 * P);
@@ -346,6 +331,8 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
+    static const std::string name = kernel_name("pair_scan_kernel", P, MINB, MM, X);
+    t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),
         (const LayerTermsT<double> *)st.d_terms, st.n_layers);

@@ -75,8 +75,12 @@ def test_bench_json_line_on_gpu():
         assert k in d, k
     assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3 and d["dtype"] == "f64"
     r = d["roofline"]
-    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
-    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert r["bound"] == "l2_gather" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and 0 < r["frac"] <= 1.05
+    assert r["north_star"]["bound"] == "hbm" and r["north_star_frac"] > 0
+    assert r["kernel"].startswith(("pair_scan_kernel<", "scan_kernel<"))
+    p = d["parity"]  # every YLT entry of the last timed step against the oracle
+    assert p["pass"] and p["ylt_mismatches"] == 0 and p["ylt_n"] == 100_000 and p["pml_exact"]
     assert d["gpu_launches"] >= 3 * 3  # probe / length check or sort, scan, metrics per step
     assert d["e2e"]["h2d_bytes_per_step"] > 4 * 10**8 and d["e2e"]["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1

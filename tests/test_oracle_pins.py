@@ -460,6 +460,44 @@ def test_f32_separate_rounding():
         assert oracle.apply_financial_terms_f32(float(xi), float(ri), float(ti), math.inf) == want
 
 
+def _f32_accumulation_dataset():
+    """Float-exact inputs whose float and double accumulations differ: 2^24 + 1 is not a float
+    (it rounds to 2^24, ties to even).  Trial 0 = [1, 2, 2]: event 1's ELT sum 2^24 + 1 (lines
+    11-13); trial 1 = [3, 4, 4]: exact per-event losses 2^24, 1, 1 whose running sum S (line 19)
+    passes 2^24 + 1.  Identity terms, so lr = S."""
+    big = float(2 ** 24)
+    elts = [{"records": [(1, big), (2, 1.0), (3, big)], "fin": (1.0, 0.0, math.inf)},
+            {"records": [(1, 1.0), (2, 1.0), (4, 1.0)], "fin": (1.0, 0.0, math.inf)}]
+    layers = [{"elts": [0, 1], "terms": (0.0, math.inf, 0.0, math.inf)}]
+    return make_dataset(8, elts, layers, [[1, 2, 2], [3, 4, 4]])
+
+
+def test_f32_accumulates_in_float():
+    """F3 accumulation precision: the expected values are computed with numpy float32 IEEE ops,
+    the same sequence as Alg. 1 lines 11-28 in float; an instantiation that
+    silently accumulated the ELT sum or S in double would give the fp64 values instead."""
+    f = np.float32
+    ds = _f32_accumulation_dataset()
+    # trial 0: lo_1 = f(2^24) + f(1) = 2^24 (rounded), lo_2 = 2; S: 2^24, 2^24 + 2, 2^24 + 4
+    lo = [f(f(f(0) + f(2 ** 24)) + f(1)), f(f(f(0) + f(1)) + f(1)), f(f(f(0) + f(1)) + f(1))]
+    S, lr, prev = f(0), f(0), f(0)
+    for x in lo:
+        S = f(S + x)
+        lr = f(lr + f(S - prev))
+        prev = S
+    want0 = float(lr)
+    # trial 1: per-event losses 2^24, 1, 1 (exact); S rounds at 2^24 + 1 -> 2^24, twice
+    S = f(0)
+    for x in (f(2 ** 24), f(1), f(1)):
+        S = f(S + x)
+    want1 = float(S)
+    y32 = oracle.run_analysis(ds, precision=32)[0]
+    y64 = oracle.run_analysis(ds)[0]
+    assert want0 == 2 ** 24 + 4 and want1 == 2 ** 24
+    assert y32.tolist() == [want0, want1]
+    assert y64.tolist() == [2 ** 24 + 5, 2 ** 24 + 2]  # double accumulation: different
+
+
 def test_f32_within_rounding_bound_of_f64():
     """fp32 vs fp64 on generated data: |y32 - y64| within the absolute rounding bound of float
     arithmetic over the trial, c (k + E + 2) u32 (S + AggR), u32 = 2^-24 (input rounding
@@ -496,3 +534,33 @@ def test_portfolio_row_pins():
     # monotone: adding a layer never lowers a trial's portfolio loss (all entries >= 0)
     y = rng.lognormal(5, 3, (4, 50))
     assert (oracle.portfolio_row(y) >= oracle.portfolio_row(y[:3])).all()
+
+
+# --------------------------------------------------------------------------- F4 EP curves
+def test_ep_curve_pins():
+    """Exceedance-probability curve (F4, reading R15): SPEC's 1..100 row gives 100, 99, ..., 1
+    and its PML(0.99) = 99 sits at rank n - ceil(p n); on random rows with ties
+    the curve is non-increasing, a permutation of the row (numpy's sort, an independent library
+    routine), every entry i has at least i + 1 values >= it and at most i values > it (brute
+    force), and the nearest-rank PML of every return period is a point on it."""
+    v = np.arange(1.0, 101.0)
+    rng = np.random.default_rng(15)
+    c = oracle.ep_curve(rng.permutation(v))
+    assert c.tolist() == list(np.arange(100.0, 0.0, -1.0))
+    assert c[100 - math.ceil(0.99 * 100)] == oracle.metrics(v, [0.99])[0][0] == 99.0
+    p = [1 - 1 / rp for rp in (10, 25, 50, 100, 250, 500, 1000)]
+    for trial in range(200):
+        n = int(rng.integers(1, 400))
+        row = np.round(rng.lognormal(3, 2, n), 1 if trial % 2 else 8)  # ties when rounded
+        c = oracle.ep_curve(row)
+        assert (np.diff(c) <= 0).all()
+        assert np.array_equal(np.sort(row)[::-1], c)
+        if n <= 60:
+            for i in range(n):
+                assert (row >= c[i]).sum() >= i + 1 and (row > c[i]).sum() <= i
+        pml = oracle.metrics(row, p)[0]
+        for pi, q in zip(p, pml):
+            assert c[n - math.ceil(pi * n)] == q
+    assert oracle.ep_curve(np.array([7.5])).tolist() == [7.5]
+    with pytest.raises(ValueError):
+        oracle.ep_curve(np.array([]))

@@ -3,13 +3,19 @@
 `ncu --set full` capture of a scan or portfolio launch.
 
     python tools/ncu_traffic.py CONFIG REPORT.ncu-rep N_TRIALS "bound text" [--source TEXT]
+                                [--lib paper_1308_2572_b200/libara.so]
 
-Reads the report's raw page (ncu -i ... --page raw --csv) and stores, per config: DRAM bytes per
-launch (dram__bytes_read.sum + dram__bytes_write.sum), L1 data-pipe / L2 / fp64 / ALU / issue
-utilisation and the duration under ncu.
+Reads the report's raw page (ncu -i ... --page raw --csv) and stores DRAM bytes per launch
+(dram__bytes_read.sum + dram__bytes_write.sum), L1 data-pipe / L1->L2 request / L2 / fp64 / ALU /
+issue utilisation and the duration under ncu, keyed "<kernel instantiation>|<sha256[:16] of the
+libara.so that ran>|<config>": bench.py reports an entry only for the same kernel of the same
+build, so a changed kernel never shows stale counters.  Run it on the report of the library
+that is committed alongside (the .so is rebuilt from the committed sources).
 """
 import csv
+import hashlib
 import io
+import re
 import json
 import os
 import subprocess
@@ -42,15 +48,23 @@ def pct(d, key):
 def main():
     cfg, report, n_trials, bound = sys.argv[1:5]
     src = sys.argv[sys.argv.index("--source") + 1] if "--source" in sys.argv else report
+    lib = sys.argv[sys.argv.index("--lib") + 1] if "--lib" in sys.argv else os.path.join(
+        ROOT, "paper_1308_2572_b200", "libara.so")
+    sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
     d = raw(report)
+    m = re.search(r"(\w+<[^()]*>)\(", d["Kernel Name"][0])
+    kern = m.group(1) if m else d["Kernel Name"][0]
     entry = {
-        "kernel": d["Kernel Name"][0][:120],
+        "kernel": kern,
+        "lib_sha16": sha,
         "n_trials": int(n_trials),
         "dram_bytes_per_launch": num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum"),
         "l2_to_l1_bytes": num(d, "l1tex__m_xbar2l1tex_read_bytes.sum"),
         "l2_hit_rate": pct(d, "lts__t_sector_hit_rate.pct"),
         "l1_data_pipe_busy": pct(d, "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+        "l1_to_l2_request_busy": pct(d, "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"),
         "lts_throughput": pct(d, "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+        "warps_per_sm": num(d, "sm__warps_active.avg.per_cycle_active"),
         "fp64_pipe": pct(d, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "alu_pipe": pct(d, "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
         "issue_active": pct(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
@@ -59,7 +73,8 @@ def main():
         "bound": bound,
     }
     j = json.load(open(OUT)) if os.path.exists(OUT) else {}
-    j[cfg] = entry
+    j = {k: v for k, v in j.items() if "|" in k or k == "source"}  # round-1 keys were stale
+    j[f"{kern}|{sha}|{cfg}"] = entry
     j["source"] = src
     with open(OUT, "w") as f:
         json.dump(j, f, indent=1)
