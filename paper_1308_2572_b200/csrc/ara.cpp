@@ -782,10 +782,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
         if (const char *d = getenv("ARA_SCAN_DEPTH")) st.depth = atoi(d);
-        if (const char *q = getenv("ARA_PAIR_SCAN")) {
-            st.pair_scan = atoi(q) != 0;
-            st.pair_scan_wide = atoi(q) == 2;
-        }
+        if (const char *q = getenv("ARA_PAIR_SCAN")) st.pair_scan = atoi(q) != 0;
         st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
                                                        elt_index);
         std::vector<uint32_t> map((size_t)C + 1, 0u);

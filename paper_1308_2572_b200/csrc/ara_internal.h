@@ -109,11 +109,10 @@ struct DeviceStore {
     int group_override = 0;      // tuning: G for W = 16 (env ARA_SCAN_GROUP), 0 = default
     int min_blocks = 0;          // tuning: __launch_bounds__ min blocks (env ARA_SCAN_MINB)
     int depth = 0;               // tuning: rows in flight per group (env ARA_SCAN_DEPTH)
-    // scan_pair.cu (fp64, W = 16 / 32 / 64): every loss * rate, retention, finite limit and
+    // scan_pair.cu (fp64, W = 16 / 32): every loss * rate, retention, finite limit and
     // layer term is below 2^960, so the exactly scaled clamps cannot overflow
     bool scaled = false;
     bool pair_scan = true;       // tuning: ARA_PAIR_SCAN=0 runs scan.cu's kernel instead
-    bool pair_scan_wide = false; // tuning: ARA_PAIR_SCAN=2 also for W = 32 / 64
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     // Row addressing of the scan: 0 = through d_map (dense rows);
     // 1 = direct (rows indexed by catalogue id, no map read); 2 = direct behind a presence

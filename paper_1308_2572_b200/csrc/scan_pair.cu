@@ -3,19 +3,14 @@
 //
 // Decomposition.  A row of W = 16 P doubles is P 128-byte lines.  A group of G = 2 P lanes owns
 // one (trial, layer) ticket; lane c owns the 8 columns [8c, 8c + 8) of the layer's row (two
-// 256-bit loads), so pair p = (lanes 2p, 2p + 1) covers line p and each of its load instructions
-// touches one line per pair -- the same L1 wavefront cost per line as the 16-column kernel.  The
-// ELT sum of lines 11-13 must be the oracle's ((0 + F_0) + F_1) + ... + F_{W-1} (SURVEY.md
-// finding 3), i.e. a chain through the lanes in column order.  Pair p works one event behind
-// pair p - 1 ("skew"): at step s lane c processes event s - floor(c / 2), so in every step
-// phase A (even lanes: the first 8 columns of their line) and phase B (odd lanes: the last 8,
-// continuing from the even lane's partial) all P pairs advance their own event in the same two
-// phases.  The partial of event e leaves pair p at the end of step s and enters pair p + 1 at
-// step s + 1, when pair p + 1 has event e's line in its registers.  Per step the group issues
-// 16 ordered adds per lane whatever P is (the unskewed chain needs 8 P), and the loads of a step
-// touch P lines -- one per pair -- exactly as without the skew.  The row index of pair p at step
-// s is pair p - 1's index at step s - 1 (one shuffle); a trial takes k + P - 1 steps, the first
-// and last P - 1 of them reading zero rows on the idle pairs (exact no-ops, reading R12).
+// 256-bit loads per event, both lines of a row in the same instructions).  The ELT sum of lines
+// 11-13 must be the oracle's ((0 + F_0) + F_1) + ... + F_{W-1} (SURVEY.md finding 3), i.e. a
+// chain through the lanes in column order: lane 0 sums its 8 columns, each further lane adds its
+// 8 columns to its left neighbour's partial after one 64-bit shuffle (G - 1 hops; in SIMT every
+// lane issues every hop).  P = 1 (the paper's 15-16 ELT layers) is the headline kernel; P = 2
+// serves 17-32 ELTs.  (A skewed variant -- pair p one or two events behind pair p - 1, so every
+// step needs only two hops -- computed fewer adds but ran 1.4-1.6x slower: its gathers were
+// scheduled too late under register pressure; profiles/r2_tune_pair.jsonl.)
 //
 // Exactly scaled clamps.  sm_100a has no fp64 min/max instruction; max(x, 0) as a compare-select
 // costs DSETP + 2 FSEL.  Instead the kernel carries power-of-two multiples of the oracle's values:
@@ -75,40 +70,34 @@ struct TrialState {
     double S4, C8, lr8, max4;
 };
 
-// One step of lane c on its row segment r (event s - c/2): financial terms of its 8 columns,
-// phase A / phase B of the ELT chain, then (meaningful in lane G - 1) the occurrence and
-// aggregate terms.  xB carries the lane's phase-B partial to the next step (P > 1); own is the
-// lane's phase-A value (the gather pin).  Returns inc8 (lane G - 1).
+// One step of lane c on its row segment r: financial terms of its 8 columns, the ELT chain,
+// then (meaningful in lane G - 1) the occurrence and aggregate terms.  own is the lane's partial
+// of its own columns (the gather pin).  Returns inc8 (lane G - 1).
 template <int P>
 __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
-                                            uint32_t c, uint32_t gmask, double &xB, double &own,
-                                            TrialState &st)
+                                            uint32_t gmask, double &own, TrialState &st)
 {
     constexpr int G = 2 * P;
     double f[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const double x = rsub(rmul(r[j >> 2].v[j & 3], T.rate[j]), T.ret[j]);  // line 9
-        f[j] = cmin(j < ARA_PAIR_INTMAX ? int_max0(x) : twice_max0(x), T.lim2[j]);
+        f[j] = cmin(twice_max0(x), T.lim2[j]);
     }
-    double a;
-    if constexpr (P == 1) {  // lane 0 starts the chain at F2_0 (= 0 + F2_0)
-        a = f[0];
+    // lines 11-13: lane 0 starts at F2_0 (= 0 + F2_0), lane h continues lane h - 1's partial
+    double a = f[0];
 #pragma unroll
-        for (int j = 1; j < 8; ++j) a = radd(a, f[j]);
-    } else {  // even lane 2p > 0 continues event s - p from lane 2p - 1's last phase B
-        const double in = __shfl_up_sync(gmask, xB, 1, G);
-        a = (c == 0) ? 0.0 : in;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a = radd(a, f[j]);
-    }
+    for (int j = 1; j < 8; ++j) a = radd(a, f[j]);
     own = a;
-    double b = __shfl_up_sync(gmask, a, 1, G);  // odd lane 2p + 1 continues lane 2p's partial
 #pragma unroll
-    for (int j = 0; j < 8; ++j) b = radd(b, f[j]);
-    xB = b;
-    // lines 15-29 on lo2 = b (lane G - 1)
-    const double t2 = rsub(b, T.occ_ret2);
+    for (int h = 1; h < G; ++h) {
+        double x = __shfl_up_sync(gmask, a, 1, G);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x = radd(x, f[j]);
+        a = x;
+    }
+    // lines 15-29 on lo2 = a (lane G - 1)
+    const double t2 = rsub(a, T.occ_ret2);
     const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
     st.S4 = radd(st.S4, oc4);
     const double u4 = rsub(st.S4, T.agg_ret4);
@@ -128,21 +117,40 @@ __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint
     load_row_chunk(p + 4, r[1]);
 }
 
-// Row index of this lane for the next step: pair 0 from its own event id, pair p > 0 takes pair
-// p - 1's index of the current step.
-template <int P>
-__device__ __forceinline__ uint32_t next_index(uint32_t idx0, uint32_t cur, uint32_t c,
-                                               uint32_t gmask)
+// F4 increments of an aligned 8-event chunk: the writer lane stages inc_d in shared memory and
+// the group stores the chunk as one 64-byte segment (8 / G doubles per lane, streaming hint)
+// instead of 8 scattered 8-byte stores.
+template <int G>
+__device__ __forceinline__ void flush_chunk(const double *stage, double *dst, uint32_t c,
+                                            uint32_t gmask)
 {
-    if constexpr (P == 1) {
-        (void)cur;
-        (void)c;
-        (void)gmask;
-        return idx0;
+    constexpr int PER = 8 / G;
+    __syncwarp(gmask);  // the writer's staged values are visible to the group
+    const double *src = stage + c * PER;
+    double *d = dst + c * PER;
+    if ((((uintptr_t)dst) & 63u) == 0 && PER == 4) {
+        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(d), "d"(src[0]),
+                     "d"(src[1]), "d"(src[2]), "d"(src[3])
+                     : "memory");
+    } else if ((((uintptr_t)dst) & 63u) == 0 && PER == 2) {
+        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(d), "d"(src[0]), "d"(src[1])
+                     : "memory");
     } else {
-        const uint32_t up = __shfl_up_sync(gmask, cur, 2, 2 * P);
-        return c < 2 ? idx0 : up;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) d[k] = src[k];
     }
+    __syncwarp(gmask);  // the stage is read before the next chunk overwrites it
+}
+
+// Row index of the event at step J of the current 8-event chunk (J = 8, 9: the next chunk; past
+// the last full chunk the prefetch reads a zero row -- the tail redoes those steps).
+template <int MM>
+__device__ __forceinline__ uint32_t chunk_row(int J, const uint32_t (&idc)[8],
+                                              const uint32_t (&idn)[8], bool more,
+                                              const RowLookup &look, bool &bad)
+{
+    if (J < 8) return row_index<MM>(look, idc[J < 8 ? J : 0], bad);
+    return more ? row_index<MM>(look, idn[J - 8 < 8 ? J - 8 : 0], bad) : look.zero_base;
 }
 
 template <int P, int MM, int X>
@@ -155,6 +163,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
     constexpr int G = 2 * P;
+    __shared__ __align__(16) double s_inc[X == 2 ? (kScanThreads / G) * 8 : 2];  // F4 staging
     constexpr uint32_t W = 16 * P;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;
@@ -207,72 +216,57 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             }
             const uint64_t beg = s.offsets[t] - base;
             const uint64_t k = s.offsets[t + 1] - base - beg;
-            const uint32_t *ev = s.ids + beg;
-            const uint32_t *const ev_end = ev + k;
+            const uint32_t *const tr = s.ids + beg;  // the trial's event ids
             TrialState st{0.0, 0.0, 0.0, 0.0};
-            double xB = 0.0, own = 0.0;
-            uint32_t cur = zb;  // index of the last step's row (pipeline fill: zero rows)
-            // F4 increments: lane G - 1 at the step whose pair-0 event sits at YET position pos0
-            // finishes the event at pos0 - (P - 1); the first P - 1 steps finish no event
-            const uint64_t first_pos = beg + (P - 1);
-            auto out = [&](double inc8, uint64_t pos0) {
+            double own = 0.0;
+            auto out = [&](double inc8, uint64_t e) {  // F4: the increment of event e
                 if constexpr (X == 2)
-                    if (inc_row && writer && pos0 >= first_pos) inc_row[pos0 - (P - 1)] = inc8 * 0.125;
+                    if (inc_row && writer) inc_row[beg + e] = inc8 * 0.125;
             };
-            auto single = [&](uint32_t idx0, uint64_t pos0) {
-                const uint32_t idx = next_index<P>(idx0, cur, c, gmask);
-                cur = idx;
+            auto single = [&](uint64_t e) {
                 Chunk<double> r[2];
-                gather2(my_rows, row_stride, idx, r);
-                out(pair_step<P>(r, T, c, gmask, xB, own, st), pos0);
+                gather2(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
+                out(pair_step<P>(r, T, gmask, own, st), e);
             };
+            uint64_t e = 0;
             // head: single events until the id pointer is 32-byte aligned
-            while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
-                single(row_index<MM>(look, load_id(ev), bad), (uint64_t)(ev - s.ids));
-                ++ev;
-            }
+            while (e < k && (((uintptr_t)(tr + e)) & 31u) != 0) single(e++);
             // body: chunks of 8 events; the ids of chunk i + 1 are in flight during chunk i, the
-            // gather of step j + 1 while step j is computed
-            const uint64_t n_chunks = (uint64_t)(ev_end - ev) / 8;
+            // gather of event j + 1 while event j is computed
+            const uint64_t n_chunks = (k - e) / 8;
+            double *const stage = (X == 2 && inc_row) ? s_inc + (threadIdx.x / G) * 8 : nullptr;
+            auto out8 = [&](double inc8, int j) {  // body events: staged
+                if constexpr (X == 2)
+                    if (stage && writer) stage[j] = inc8 * 0.125;
+            };
             if (n_chunks) {
                 uint32_t id_c[8], id_n[8];
-                load_ids8(ev, id_c);
-                if (n_chunks > 1) load_ids8(ev + 8, id_n);
-                uint32_t ia = next_index<P>(row_index<MM>(look, id_c[0], bad), cur, c, gmask);
+                load_ids8(tr + e, id_c);
+                if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
                 Chunk<double> ra[2], rb[2];
-                gather2(my_rows, row_stride, ia, ra);
-                uint64_t pos = (uint64_t)(ev - s.ids);
+                gather2(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
+                    const uint64_t e0 = e + 8 * i;
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
-                        const uint32_t ib = next_index<P>(row_index<MM>(look, id_c[j + 1], bad), ia, c, gmask);
+                        const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
                         gather2(my_rows, row_stride, pin(ib, own), rb);
-                        out(pair_step<P>(ra, T, c, gmask, xB, own, st), pos + j);
-                        const uint32_t id2 = j + 2 < 8 ? id_c[j + 2 < 8 ? j + 2 : 0] : id_n[0];
-                        const bool ok2 = j + 2 < 8 || more;
-                        const uint32_t ic =
-                            next_index<P>(ok2 ? row_index<MM>(look, id2, bad) : zb, ib, c, gmask);
+                        out8(pair_step<P>(ra, T, gmask, own, st), j);
+                        const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
                         gather2(my_rows, row_stride, pin(ic, own), ra);
-                        out(pair_step<P>(rb, T, c, gmask, xB, own, st), pos + j + 1);
-                        cur = ib;
-                        ia = ic;
+                        out8(pair_step<P>(rb, T, gmask, own, st), j + 1);
                     }
+                    if constexpr (X == 2)
+                        if (stage) flush_chunk<G>(stage, inc_row + beg + e0, c, gmask);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
-                    if (i + 2 < n_chunks) load_ids8(ev + 8 * (i + 2), id_n);
-                    pos += 8;
+                    if (i + 2 < n_chunks) load_ids8(tr + e + 8 * (i + 2), id_n);
                 }
-                ev += 8 * n_chunks;
+                e += 8 * n_chunks;
             }
-            // tail: remaining events one by one, then the P - 1 drain steps (pair 0 idle)
-            while (ev < ev_end) {
-                single(row_index<MM>(look, load_id(ev), bad), (uint64_t)(ev - s.ids));
-                ++ev;
-            }
-#pragma unroll
-            for (int d = 0; d < P - 1; ++d) single(zb + d, (uint64_t)(ev_end - s.ids) + d);
+            while (e < k) single(e++);  // tail
             if (writer) {
                 ylt_row[t] = st.lr8 * 0.125;  // A8 (exact rescale)
                 if (X && mo_row) mo_row[t] = st.max4 * 0.25;
@@ -364,11 +358,10 @@ cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_cou
 
 bool pair_scan_eligible(const DeviceStore &st, const ScanLaunch &s)
 {
-    // W = 32 / 64 (P > 1) serialise consecutive steps through the skewed chain: measured 1.5-1.7x
-    // slower than scan.cu's unskewed G = 4 kernel (profiles/r2_tune_pair.jsonl); tuning only
-    const bool wide_ok = st.pair_scan_wide && (st.width == 32 || st.width == 64);
+    // W = 64: scan.cu's G = 4 lanes x 16 columns is faster (61.8 vs 72.7 ms for 1M x 1000,
+    // profiles/r2_tune_pair.jsonl): 8 lanes x 8 columns issue twice the chain adds
     return st.bits == 64 && st.scaled && s.counter && s.done && st.pair_scan &&
-           (st.width == 16 || wide_ok);
+           (st.width == 16 || st.width == 32);
 }
 
 cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
@@ -377,11 +370,8 @@ cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
     switch (st.width) {
-        case 16:
-            if (st.min_blocks == 4) return launch_pair_x<1, 4>(st, s, sm_count, stream);
-            return launch_pair_x<1, 3>(st, s, sm_count, stream);
+        case 16: return launch_pair_x<1, 3>(st, s, sm_count, stream);
         case 32: return launch_pair_x<2, 3>(st, s, sm_count, stream);
-        case 64: return launch_pair_x<4, 3>(st, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
     }
 }
