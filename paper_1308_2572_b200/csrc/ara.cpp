@@ -496,6 +496,7 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     ara::UnionStore &us = st.uni;
     us.GU = GU;
     us.shfl = shfl ? (full16 ? 2 : 1) : 0;
+    us.scaled = st.scaled && st.pair_scan;  // ARA_PAIR_SCAN=0 also keeps the compare-selects
     us.n_cols = (uint32_t)J.size();
     us.zero_base = st.n_union + 1;
     const size_t row_bytes = rows.size() * 8;

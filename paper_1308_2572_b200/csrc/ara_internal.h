@@ -93,6 +93,7 @@ struct UnionStore {
     int shfl = 0;            // layer sums: 0 = shared-memory F row; 1 = register shuffles
                              // (general); 2 = register shuffles, every layer has 16 ELTs
     uint32_t n_cols = 0;     // |J|
+    bool scaled = false;     // DeviceStore::scaled (the scaled-clamp instantiation may run)
     double *d_rows = nullptr;            // [(U+1+kZeroRows) * WU]
     UnionTermsDev *d_terms = nullptr;
 };

@@ -23,6 +23,10 @@
 // lane src(l, i): each position is one 64-bit shuffle per group, with no shared-memory writes,
 // reads or barriers (the shared F row cost 2 L1 wavefronts per trial-layer-event, the shuffles
 // cost 1).  SH = 2: every layer has 16 ELTs; SH = 1: shorter layers add +0 past their end.
+//
+// SC = 1: the exactly scaled clamps of scan_pair.cu (reading R16): F2 = min(x + |x|,
+// 2 lim), lo2, oc4, S4, C8, lr8, YLT = lr8 * 0.125 -- the oracle's bits with one DADD per clamp
+// instead of DSETP + 2 FSEL (inputs below 2^960, UnionStore::scaled).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,7 +47,10 @@ __host__ __device__ constexpr int u_row_doubles()
     return (u_slot(8 * GU) + 2 + 15) / 16 * 16 + 1;
 }
 
-template <int GU, bool BAL, int MM, int SH>
+__device__ __forceinline__ double twice_max0(double x) { return __dadd_rn(x, fabs(x)); }
+__device__ __forceinline__ double cmin(double m, double lim) { return (lim < m) ? lim : m; }
+
+template <int GU, bool BAL, int MM, int SH, int SC>
 __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
                                                const uint32_t *__restrict__ map,
                                                const uint32_t *__restrict__ bitmap,
@@ -76,14 +83,17 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
             const int col = 4 * (c + GU * h) + q;
             rate[4 * h + q] = ut->rate[col];
             ret[4 * h + q] = ut->ret[col];
-            lim[4 * h + q] = ut->lim[col];
+            lim[4 * h + q] = (SC ? 2.0 : 1.0) * ut->lim[col];  // SC: 2 lim
         }
     // this lane's layer (lane c -> layer c): terms and the shared-memory slots of its columns
     const uint32_t n_layers = ut->n_layers;
     const bool has_layer = c < n_layers;
     const uint32_t ly = has_layer ? c : 0;
-    const double occ_ret = ut->occ_ret[ly], occ_lim = ut->occ_lim[ly];
-    const double agg_ret = ut->agg_ret[ly], agg_lim = ut->agg_lim[ly];
+    // SC: 2 OccR, 4 OccL, 4 AggR, 8 AggL (the scaled domain of reading R16)
+    const double occ_ret = (SC ? 2.0 : 1.0) * ut->occ_ret[ly];
+    const double occ_lim = (SC ? 4.0 : 1.0) * ut->occ_lim[ly];
+    const double agg_ret = (SC ? 4.0 : 1.0) * ut->agg_ret[ly];
+    const double agg_lim = (SC ? 8.0 : 1.0) * ut->agg_lim[ly];
     uint32_t slot2[SH == 0 ? kUnionMaxE / 2 : 1];  // two 16-bit slots per register
     if constexpr (SH == 0) {
 #pragma unroll
@@ -113,7 +123,7 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
             for (int q = 0; q < 4; ++q) {
                 const int j = 4 * h + q;
                 const double l = rsub(rmul(r[h].v[q], rate[j]), ret[j]);  // line 9
-                f[j] = dmin(dmax0(l), lim[j]);
+                f[j] = SC ? cmin(twice_max0(l), lim[j]) : dmin(dmax0(l), lim[j]);
             }
         double lo = 0.0;  // lines 11-13 for this lane's layer, in the layer's ELT order
         if constexpr (SH == 0) {
@@ -153,9 +163,11 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
             }
         }
         own = lo;  // (pinning the gathers on lo instead of S measured 4% slower here)
-        const double oc = dmin(dmax0(rsub(lo, occ_ret)), occ_lim);  // line 16
-        S = radd(S, oc);                                              // line 19
-        const double Cd = dmin(dmax0(rsub(S, agg_ret)), agg_lim);     // line 22
+        const double t = rsub(lo, occ_ret);
+        const double oc = SC ? cmin(twice_max0(t), occ_lim) : dmin(dmax0(t), occ_lim);  // l. 16
+        S = radd(S, oc);                                                                // l. 19
+        const double u = rsub(S, agg_ret);
+        const double Cd = SC ? cmin(twice_max0(u), agg_lim) : dmin(dmax0(u), agg_lim);  // l. 22
         lr = radd(lr, rsub(Cd, Cprev));                               // lines 25, 28
         Cprev = Cd;
     };
@@ -225,7 +237,7 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
                 event(r, S, Cprev, lr, own);
                 ++ev;
             }
-            if (has_layer) ylt_row[t] = lr;  // A8, one entry per layer
+            if (has_layer) ylt_row[t] = SC ? lr * 0.125 : lr;  // A8, one entry per layer
         }
         if (BAL) {
             __syncwarp();
@@ -255,7 +267,7 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
 }
 
 // Map mode 2 runs the mode-1 body when the hit probe found (nearly) every sampled id present.
-template <int GU, bool BAL, int MM, int SH>
+template <int GU, bool BAL, int MM, int SH, int SC>
 __global__ void __launch_bounds__(kScanThreads, 3)
     portfolio_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                      const uint32_t *__restrict__ bitmap, const double *__restrict__ urows,
@@ -263,21 +275,21 @@ __global__ void __launch_bounds__(kScanThreads, 3)
 {
     if constexpr (MM == 2) {
         if (!probe_use_bitmap(s.probe)) {
-            portfolio_body<GU, BAL, 1, SH>(s, map, bitmap, urows, ut);
+            portfolio_body<GU, BAL, 1, SH, SC>(s, map, bitmap, urows, ut);
             return;
         }
     }
-    portfolio_body<GU, BAL, MM, SH>(s, map, bitmap, urows, ut);
+    portfolio_body<GU, BAL, MM, SH, SC>(s, map, bitmap, urows, ut);
 }
 
-template <int GU, bool BAL, int MM, int SH>
+template <int GU, bool BAL, int MM, int SH, int SC>
 cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32_t *d_bitmap,
                        const ScanLaunch &s, int sm_count, cudaStream_t stream)
 {
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Union) : 0;
     static std::atomic<int> occ_cache[kMaxDevices];  // resident blocks per SM, per device
     int occ = 0;
-    cudaError_t oe = blocks_per_sm((const void *)portfolio_kernel<GU, BAL, MM, SH>,
+    cudaError_t oe = blocks_per_sm((const void *)portfolio_kernel<GU, BAL, MM, SH, SC>,
                                    kScanThreads, smem, occ_cache, occ);
     if (oe != cudaSuccess) return oe;
     const uint64_t per_block = kScanThreads / GU;
@@ -290,21 +302,21 @@ cudaError_t launch_pum(const UnionStore &us, const uint32_t *d_map, const uint32
     ScanLaunch sl = s;
     sl.zero_base = MM ? us.zero_base_direct : us.zero_base;
     sl.bitmap_log2 = kBitmapLog2Union;
-    static const std::string name = kernel_name("portfolio_kernel", GU, BAL, MM, SH);
+    static const std::string name = kernel_name("portfolio_kernel", GU, BAL, MM, SH, SC);
     t_last_kernel = name.c_str();
-    portfolio_kernel<GU, BAL, MM, SH><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
+    portfolio_kernel<GU, BAL, MM, SH, SC><<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, d_map, d_bitmap, MM ? us.d_rows_direct : us.d_rows, us.d_terms);
     return cudaGetLastError();
 }
 
-template <int GU, bool BAL, int SH>
+template <int GU, bool BAL, int SH, int SC>
 cudaError_t launch_pus(const UnionStore &us, const uint32_t *d_map, int map_mode,
                        const uint32_t *d_bitmap, const ScanLaunch &s, int sm_count,
                        cudaStream_t stream)
 {
-    if (map_mode == 1) return launch_pum<GU, BAL, 1, SH>(us, d_map, d_bitmap, s, sm_count, stream);
-    if (map_mode == 2) return launch_pum<GU, BAL, 2, SH>(us, d_map, d_bitmap, s, sm_count, stream);
-    return launch_pum<GU, BAL, 0, SH>(us, d_map, d_bitmap, s, sm_count, stream);
+    if (map_mode == 1) return launch_pum<GU, BAL, 1, SH, SC>(us, d_map, d_bitmap, s, sm_count, stream);
+    if (map_mode == 2) return launch_pum<GU, BAL, 2, SH, SC>(us, d_map, d_bitmap, s, sm_count, stream);
+    return launch_pum<GU, BAL, 0, SH, SC>(us, d_map, d_bitmap, s, sm_count, stream);
 }
 
 // Layer-sum variant (UnionStore::shfl); the shuffle variants are built for GU = 8 (up to 64
@@ -315,12 +327,17 @@ cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, int map_mode,
                       cudaStream_t stream)
 {
     if constexpr (GU == 8) {
-        if (us.shfl == 2)
-            return launch_pus<GU, BAL, 2>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        if (us.shfl == 2) {  // configuration P: the scaled clamps when the inputs allow them
+            if constexpr (BAL)
+                if (us.scaled)
+                    return launch_pus<GU, BAL, 2, 1>(us, d_map, map_mode, d_bitmap, s, sm_count,
+                                                     stream);
+            return launch_pus<GU, BAL, 2, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        }
         if (us.shfl == 1)
-            return launch_pus<GU, BAL, 1>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+            return launch_pus<GU, BAL, 1, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
     }
-    return launch_pus<GU, BAL, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+    return launch_pus<GU, BAL, 0, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
 }
 
 }  // namespace
