@@ -354,8 +354,8 @@ void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vecto
         for (uint32_t c = 0; c < E; ++c) {
             const uint32_t j = elt_index[elt_offsets[l] + c];
             for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
-                rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W + c] =
-                    (R)ctx->rec_losses[r];
+                rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W +
+                     ara::row_phys_col(c, W, st.bits)] = (R)ctx->rec_losses[r];
             lt[l].rate[c] = (R)ctx->fin[j].rate;
             lt[l].ret[c] = (R)ctx->fin[j].retention;
             lt[l].lim[c] = (R)ctx->fin[j].limit;
@@ -1184,10 +1184,14 @@ ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, doubl
                                        (const char *)st.d_rows + (size_t)layer * st.width * es,
                                        (size_t)st.n_layers * st.width * es, (size_t)st.width * es,
                                        st.n_union + 1, cudaMemcpyDeviceToHost));
-            const size_t cnt = (size_t)(st.n_union + 1) * st.width;
-            for (size_t i = 0; i < cnt; ++i)
-                h_rows[i] = st.bits == 32 ? (double)((const float *)tmp.data())[i]
-                                          : ((const double *)tmp.data())[i];
+            // logical column order (the device rows of W >= 32 are lane-interleaved)
+            for (size_t u = 0; u <= st.n_union; ++u)
+                for (uint32_t j = 0; j < st.width; ++j) {
+                    const size_t i = u * st.width + ara::row_phys_col(j, st.width, st.bits);
+                    h_rows[u * st.width + j] = st.bits == 32
+                                                   ? (double)((const float *)tmp.data())[i]
+                                                   : ((const double *)tmp.data())[i];
+                }
         }
         return ARA_OK;
     });

@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256) hoist_oc_kernel(const R *__restrict__ row
         const R *x = rows + (size_t)u * n_layers * W + (size_t)l * W;
         R lo = R(0);  // lines 11-13: ((0 + F_0) + F_1) + ..., padded columns add +0
         for (uint32_t j = 0; j < W; ++j) {
-            const R f = dmin(dmax0(rsub(rmul(x[j], T.rate[j]), T.ret[j])), T.lim[j]);  // line 9
+            const R xj = x[row_phys_col(j, W, sizeof(R) == 8 ? 64 : 32)];
+            const R f = dmin(dmax0(rsub(rmul(xj, T.rate[j]), T.ret[j])), T.lim[j]);  // line 9
             lo = radd(lo, f);
         }
         const R o = dmin(dmax0(rsub(lo, T.occ_ret)), T.occ_lim);  // line 16

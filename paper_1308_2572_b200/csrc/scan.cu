@@ -163,7 +163,9 @@ __device__ __forceinline__ void flush_inc(const double *stage, double *dst, uint
     __syncwarp(gmask);  // the stage is read before the next chunk overwrites it
 }
 
-template <int CH, typename R>
+// Chunk i of the lane's columns sits CS chunks after chunk i - 1 (CS = 1: logical rows; CS = G:
+// lane-interleaved rows, ara_internal.h row_phys_col).
+template <int CH, typename R, int CS = 1>
 __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t stride,
                                        uint32_t idx, Chunk<R> (&r)[CH])
 {
@@ -176,7 +178,7 @@ __device__ __forceinline__ void gather(const R *__restrict__ my_rows, uint32_t s
     (void)p;
 #else
 #pragma unroll
-    for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * i, r[i]);
+    for (int i = 0; i < CH; ++i) load_row_chunk(p + Chunk<R>::N * CS * i, r[i]);
 #endif
 }
 
@@ -193,6 +195,10 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
     constexpr int PER = Chunk<R>::N;
     constexpr int W = PER * G * CH;  // row width per layer (elements)
     constexpr int NCOL = PER * CH;   // columns per lane
+    // lane-interleaved rows (fp64, W >= 32): the lane's chunks are G chunks apart
+    constexpr bool ILV = sizeof(R) == 8 && W >= 32;
+    static_assert(!ILV || G == 4, "interleaved rows are laid out for 4 lanes per trial");
+    constexpr int CS = ILV ? G : 1;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;   // this lane's position in its group
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - c));
@@ -245,7 +251,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
             occ_lim = T.occ_lim;
             agg_ret = T.agg_ret;
             agg_lim = T.agg_lim;
-            my_rows = rows + (size_t)layer * W + NCOL * c;
+            my_rows = rows + (size_t)layer * W + (ILV ? PER * c : NCOL * c);
             ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
             if (X) {
                 mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
@@ -266,7 +272,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
         // head: single events until the id pointer is 32-byte aligned
         while (ev < ev_end && ((uintptr_t)ev & 31u) != 0) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
+            gather<CH, R, CS>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc, own);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -287,7 +293,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                 Chunk<R> ring[D][CH];
 #pragma unroll
                 for (int e = 0; e < D; ++e)
-                    gather<CH, R>(my_rows, row_stride, row_index<MM>(look, id_c[e], bad),
+                    gather<CH, R, CS>(my_rows, row_stride, row_index<MM>(look, id_c[e], bad),
                                   ring[e]);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
@@ -301,7 +307,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                         const uint32_t id2 = e2 < 8 ? id_c[e2 < 8 ? e2 : 0] : id_n[e2 < 8 ? 0 : e2 - 8];
                         const bool ok2 = e2 < 8 || more;
                         const uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
-                        gather<CH, R>(my_rows, row_stride, pin(idx2, own), ring[j % D]);
+                        gather<CH, R, CS>(my_rows, row_stride, pin(idx2, own), ring[j % D]);
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
@@ -317,7 +323,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
             uint32_t idx0 = row_index<MM>(look, id_c[0], bad);
             uint32_t idx1 = row_index<MM>(look, id_c[1], bad);
             Chunk<R> ra[CH];
-            gather<CH, R>(my_rows, row_stride, idx0, ra);
+            gather<CH, R, CS>(my_rows, row_stride, idx0, ra);
 #pragma unroll 1
             for (uint64_t i = 0; i < n_chunks; ++i) {
                 const bool more = i + 1 < n_chunks;
@@ -329,7 +335,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                     const bool ok2 = j + 2 < 8 || more;
                     uint32_t idx2 = ok2 ? row_index<MM>(look, id2, bad) : zb;
                     Chunk<R> rb[CH];
-                    gather<CH, R>(my_rows, row_stride, pin(idx1, own), rb);
+                    gather<CH, R, CS>(my_rows, row_stride, pin(idx1, own), rb);
                     event_step<G, CH, R>(ra, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc, own);
                     if constexpr (X == 2)
@@ -337,7 +343,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                     else
                         event_out<X, R>(oc, inc, max_oc, inc_row, (ev - s.ids) + 8 * i + j, writer);
                     uint32_t idx3 = ok2 ? row_index<MM>(look, id3, bad) : zb;
-                    gather<CH, R>(my_rows, row_stride, pin(idx2, own), ra);  // event j+2 (zero row past end)
+                    gather<CH, R, CS>(my_rows, row_stride, pin(idx2, own), ra);  // event j+2 (zero row past end)
                     event_step<G, CH, R>(rb, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret,
                                       agg_lim, S, Cprev, lr, oc, inc, own);
                     if constexpr (X == 2)
@@ -358,7 +364,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
         // tail: remaining events one by one
         while (ev < ev_end) {
             Chunk<R> r[CH];
-            gather<CH, R>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
+            gather<CH, R, CS>(my_rows, row_stride, row_index<MM>(look, load_id(ev), bad), r);
             event_step<G, CH, R>(r, rate, ret, lim, gmask, occ_ret, occ_lim, agg_ret, agg_lim, S,
                               Cprev, lr, oc, inc, own);
             event_out<X, R>(oc, inc, max_oc, inc_row, ev - s.ids, writer);
@@ -629,15 +635,9 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
                 if (st.min_blocks == 2)
                     return launch_gc<2, 2, 2, 0, double, true>(st, s, sm_count, stream);
                 return launch_gc<2, 2, 3, 0, double, true>(st, s, sm_count, stream);
-            case 32:
-                if (st.group_override == 8)
-                    return launch_gc<8, 1, 4, 0, double, true>(st, s, sm_count, stream);
-                return launch_gc<4, 2, 3, 0, double, true>(st, s, sm_count, stream);
+            case 32: return launch_gc<4, 2, 3, 0, double, true>(st, s, sm_count, stream);
             case 48: return launch_gc<4, 3, 1, 0, double, true>(st, s, sm_count, stream);
-            case 64:
-                if (st.group_override == 8)
-                    return launch_gc<8, 2, 3, 0, double, true>(st, s, sm_count, stream);
-                return launch_gc<4, 4, 1, 0, double, true>(st, s, sm_count, stream);
+            case 64: return launch_gc<4, 4, 1, 0, double, true>(st, s, sm_count, stream);
             default: --*launches; return cudaErrorInvalidValue;
         }
     }

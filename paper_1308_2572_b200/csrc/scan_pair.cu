@@ -109,12 +109,16 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
     return inc8;
 }
 
+// The lane's two 32-byte chunks: adjacent for P = 1; G chunks apart for P = 2, whose 32-column
+// rows are lane-interleaved (ara_internal.h row_phys_col), so that each of the two load
+// instructions of a group reads one whole line.
+template <int P>
 __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
                                         uint32_t idx, Chunk<double> (&r)[2])
 {
     const double *p = my_rows + (size_t)idx * stride;
     load_row_chunk(p, r[0]);
-    load_row_chunk(p + 4, r[1]);
+    load_row_chunk(p + (P == 1 ? 4 : 4 * 2 * P), r[1]);
 }
 
 // F4 increments of an aligned 8-event chunk: the writer lane stages inc_d in shared memory and
@@ -205,7 +209,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 T.occ_lim4 = 4.0 * L.occ_lim;
                 T.agg_ret4 = 4.0 * L.agg_ret;
                 T.agg_lim8 = 8.0 * L.agg_lim;
-                my_rows = rows + (size_t)layer * W + 8 * c;
+                my_rows = rows + (size_t)layer * W + (P == 1 ? 8 * c : 4 * c);
                 ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
                 if (X) {
                     mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
@@ -225,7 +229,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             };
             auto single = [&](uint64_t e) {
                 Chunk<double> r[2];
-                gather2(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
+                gather2<P>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
                 out(pair_step<P>(r, T, gmask, own, st), e);
             };
             uint64_t e = 0;
@@ -244,7 +248,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 load_ids8(tr + e, id_c);
                 if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
                 Chunk<double> ra[2], rb[2];
-                gather2(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
+                gather2<P>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -252,10 +256,10 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
-                        gather2(my_rows, row_stride, pin(ib, own), rb);
+                        gather2<P>(my_rows, row_stride, pin(ib, own), rb);
                         out8(pair_step<P>(ra, T, gmask, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
-                        gather2(my_rows, row_stride, pin(ic, own), ra);
+                        gather2<P>(my_rows, row_stride, pin(ic, own), ra);
                         out8(pair_step<P>(rb, T, gmask, own, st), j + 1);
                     }
                     if constexpr (X == 2)
