@@ -124,18 +124,6 @@ __device__ __forceinline__ void event_out_staged(R oc, R inc, R &max_oc, double 
     if (X == 2 && stage && writer) stage[j] = (double)inc;
 }
 
-__device__ __forceinline__ void store_v2(double *p, double a, double b)
-{
-    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
-}
-
-__device__ __forceinline__ void store_v4(double *p, double a, double b, double c, double d)
-{
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
-                 "d"(d)
-                 : "memory");
-}
-
 template <int G>
 __device__ __forceinline__ void flush_inc(const double *stage, double *dst, uint32_t c,
                                           uint32_t gmask)
@@ -191,7 +179,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
-    __shared__ __align__(16) double s_inc[X == 2 ? (kScanThreads / G) * 8 : 2];  // F4 staging
+    __shared__ __align__(16) double s_inc[X == 2 ? (kScanThreads / G) * kStageStride : 2];  // F4 staging
     constexpr int PER = Chunk<R>::N;
     constexpr int W = PER * G * CH;  // row width per layer (elements)
     constexpr int NCOL = PER * CH;   // columns per lane
@@ -316,7 +304,7 @@ __device__ __forceinline__ void scan_body(const ScanLaunch &s, const uint32_t *_
                 ev += 8 * n_chunks;
             }
         } else if (n_chunks) {
-            double *const stage = (X == 2 && inc_row) ? s_inc + (threadIdx.x / G) * 8 : nullptr;
+            double *const stage = (X == 2 && inc_row) ? s_inc + (threadIdx.x / G) * kStageStride : nullptr;
             uint32_t id_c[8], id_n[8];
             load_ids8(ev, id_c);
             if (n_chunks > 1) load_ids8(ev + 8, id_n);

@@ -11,6 +11,10 @@ namespace ara {
 namespace scan_detail {
 
 constexpr int kScanThreads = 128;  // 4 warps: fine occupancy steps for 80-170 registers
+// F4 increment staging: one 8-double slot per group, padded to 9 doubles so that the writer
+// lanes' per-event 8-byte stores of the 16 groups of a warp fall in distinct bank pairs (an
+// 8-double stride put 8 groups on one bank pair: an 8-way conflict per event)
+constexpr int kStageStride = 9;
 
 // One 32-byte chunk of a row: 4 doubles (fp64 store) or 8 floats (fp32 store, F3).
 template <typename R>
@@ -19,9 +23,12 @@ struct Chunk {
     R v[N];
 };
 
+#ifndef ARA_ROWS_L2
+#define ARA_ROWS_L2 ""
+#endif
 __device__ __forceinline__ void load_row_chunk(const double *p, Chunk<double> &r)
 {
-    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate" ARA_ROWS_L2 ".v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
         : "l"(p));
 }
@@ -32,6 +39,28 @@ __device__ __forceinline__ void load_row_chunk(const float *p, Chunk<float> &r)
         : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
           "=f"(r.v[6]), "=f"(r.v[7])
         : "l"(p));
+}
+
+// F4 increment stores (8 GB at the headline): L2 evict-first, so the stream of writes does not
+// displace the L2-resident rows every event gathers (with evict-normal stores 6 GB of row
+// re-reads from DRAM appeared per launch: ncu lts__t_sectors_srcunit_tex_op_read_lookup_miss).
+__device__ __forceinline__ uint64_t l2_evict_first_policy()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void store_v2(double *p, double a, double b)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p),
+                 "d"(a), "d"(b), "l"(l2_evict_first_policy())
+                 : "memory");
+}
+__device__ __forceinline__ void store_v4(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
+                 "d"(a), "d"(b), "d"(c), "d"(d), "l"(l2_evict_first_policy())
+                 : "memory");
 }
 
 // Separately rounded arithmetic in the store's precision (no FMA contraction).

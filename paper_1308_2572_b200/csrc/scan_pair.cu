@@ -73,7 +73,7 @@ struct TrialState {
 // One step of lane c on its row segment r: financial terms of its 8 columns, the ELT chain,
 // then (meaningful in lane G - 1) the occurrence and aggregate terms.  own is the lane's partial
 // of its own columns (the gather pin).  Returns inc8 (lane G - 1).
-template <int P>
+template <int P, int X>
 __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
                                             uint32_t gmask, double &own, TrialState &st)
 {
@@ -96,7 +96,10 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
         for (int j = 0; j < 8; ++j) x = radd(x, f[j]);
         a = x;
     }
-    // lines 15-29 on lo2 = a (lane G - 1)
+    // lines 15-29 on lo2 = a (lane G - 1; with per-event increments (X == 2) every lane of the
+    // group gets lane G - 1's lo and carries the same trial state, so that each lane can keep and
+    // store its own share of the chunk's increments without shared memory)
+    if constexpr (X == 2) a = __shfl_sync(gmask, a, G - 1, G);
     const double t2 = rsub(a, T.occ_ret2);
     const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
     st.S4 = radd(st.S4, oc4);
@@ -121,29 +124,34 @@ __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint
     load_row_chunk(p + (P == 1 ? 4 : 4 * 2 * P), r[1]);
 }
 
-// F4 increments of an aligned 8-event chunk: the writer lane stages inc_d in shared memory and
-// the group stores the chunk as one 64-byte segment (8 / G doubles per lane, streaming hint)
-// instead of 8 scattered 8-byte stores.
+// F4 increments of an aligned 8-event chunk: lane c of the group holds the increments of the
+// chunk's events [c PER, c PER + PER) in registers (every lane computes every increment, see
+// pair_step) and stores them as one 8 PER-byte segment -- the group writes the chunk's 64 bytes
+// contiguously, L2 evict-first (scan_common.cuh store_v4).
 template <int G>
-__device__ __forceinline__ void flush_chunk(const double *stage, double *dst, uint32_t c,
-                                            uint32_t gmask)
+__device__ __forceinline__ void keep_inc(double (&slot)[8 / G], double inc8, int j, uint32_t c)
 {
     constexpr int PER = 8 / G;
-    __syncwarp(gmask);  // the writer's staged values are visible to the group
-    const double *src = stage + c * PER;
+    if (j / PER == (int)c) slot[j % PER] = inc8 * 0.125;
+}
+template <int G>
+__device__ __forceinline__ void store_inc(const double (&slot)[8 / G], double *dst, uint32_t c)
+{
+    constexpr int PER = 8 / G;
     double *d = dst + c * PER;
-    if ((((uintptr_t)dst) & 63u) == 0 && PER == 4) {
-        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(d), "d"(src[0]),
-                     "d"(src[1]), "d"(src[2]), "d"(src[3])
-                     : "memory");
-    } else if ((((uintptr_t)dst) & 63u) == 0 && PER == 2) {
-        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(d), "d"(src[0]), "d"(src[1])
-                     : "memory");
-    } else {
-#pragma unroll
-        for (int k = 0; k < PER; ++k) d[k] = src[k];
+    if constexpr (PER == 4) {
+        if ((((uintptr_t)dst) & 63u) == 0) {
+            store_v4(d, slot[0], slot[1], slot[2], slot[3]);
+            return;
+        }
+    } else if constexpr (PER == 2) {
+        if ((((uintptr_t)dst) & 63u) == 0) {
+            store_v2(d, slot[0], slot[1]);
+            return;
+        }
     }
-    __syncwarp(gmask);  // the stage is read before the next chunk overwrites it
+#pragma unroll
+    for (int k = 0; k < PER; ++k) d[k] = slot[k];
 }
 
 // Row index of the event at step J of the current 8-event chunk (J = 8, 9: the next chunk; past
@@ -167,7 +175,6 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
     constexpr int G = 2 * P;
-    __shared__ __align__(16) double s_inc[X == 2 ? (kScanThreads / G) * 8 : 2];  // F4 staging
     constexpr uint32_t W = 16 * P;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;
@@ -230,7 +237,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             auto single = [&](uint64_t e) {
                 Chunk<double> r[2];
                 gather2<P>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
-                out(pair_step<P>(r, T, gmask, own, st), e);
+                out(pair_step<P, X>(r, T, gmask, own, st), e);
             };
             uint64_t e = 0;
             // head: single events until the id pointer is 32-byte aligned
@@ -238,10 +245,9 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             // body: chunks of 8 events; the ids of chunk i + 1 are in flight during chunk i, the
             // gather of event j + 1 while event j is computed
             const uint64_t n_chunks = (k - e) / 8;
-            double *const stage = (X == 2 && inc_row) ? s_inc + (threadIdx.x / G) * 8 : nullptr;
-            auto out8 = [&](double inc8, int j) {  // body events: staged
-                if constexpr (X == 2)
-                    if (stage && writer) stage[j] = inc8 * 0.125;
+            double slot[8 / G];  // X == 2: this lane's share of the chunk's increments
+            auto out8 = [&](double inc8, int j) {  // body events: kept in registers
+                if constexpr (X == 2) keep_inc<G>(slot, inc8, j, c);
             };
             if (n_chunks) {
                 uint32_t id_c[8], id_n[8];
@@ -257,13 +263,13 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
                         gather2<P>(my_rows, row_stride, pin(ib, own), rb);
-                        out8(pair_step<P>(ra, T, gmask, own, st), j);
+                        out8(pair_step<P, X>(ra, T, gmask, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
                         gather2<P>(my_rows, row_stride, pin(ic, own), ra);
-                        out8(pair_step<P>(rb, T, gmask, own, st), j + 1);
+                        out8(pair_step<P, X>(rb, T, gmask, own, st), j + 1);
                     }
                     if constexpr (X == 2)
-                        if (stage) flush_chunk<G>(stage, inc_row + beg + e0, c, gmask);
+                        if (inc_row) store_inc<G>(slot, inc_row + beg + e0, c);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
                     if (i + 2 < n_chunks) load_ids8(tr + e + 8 * (i + 2), id_n);
@@ -353,7 +359,10 @@ template <int P, int MINB>
 cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                           cudaStream_t stream)
 {
-    if (s.event_inc) return launch_pair_mm<P, MINB, 2>(st, s, sm_count, stream);
+#ifndef ARA_F4_MINB
+#define ARA_F4_MINB MINB
+#endif
+    if (s.event_inc) return launch_pair_mm<P, ARA_F4_MINB, 2>(st, s, sm_count, stream);
     if (s.max_occ) return launch_pair_mm<P, MINB, 1>(st, s, sm_count, stream);
     return launch_pair_mm<P, MINB, 0>(st, s, sm_count, stream);
 }
