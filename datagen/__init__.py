@@ -117,6 +117,8 @@ PRESETS = {
 _SWEEP_TERMS = {  # occ_ret_m, occ_lim_m, agg_ret_m, agg_lim_m
     "sweep-e4": (0.2549, 4.7773, 0.6135, 0.1570), "sweep-e8": (0.4358, 3.3907, 0.5489, 0.1220),
     "sweep-e16": (0.6608, 2.9150, 0.4783, 0.0986),
+    "sweep-e20": (0.7223, 2.7687, 0.4516, 0.0930), "sweep-e24": (0.7782, 2.7582, 0.4374, 0.0902),
+    "sweep-e48": (0.9423, 2.6320, 0.3815, 0.0853),
     "sweep-e32": (0.8767, 2.7155, 0.4132, 0.0927), "sweep-e64": (0.9553, 2.5511, 0.3667, 0.0831),
     "sweep-k500": (0.6608, 2.9150, 0.4715, 0.1449), "sweep-k2000": (0.6608, 2.9150, 0.4823, 0.0710),
     "sweep-ragged": (0.6608, 2.9150, 0.4330, 0.2692), "sweep-h10": (0.6608, 2.9150, 0.0483, 0.0402),
@@ -131,7 +133,7 @@ def _sweep(name, **kw):
     PRESETS[name] = PRESETS["headline"].replace(name=name, **kw)
 
 
-for _e in (4, 8, 16, 32, 64):
+for _e in (4, 8, 16, 20, 24, 32, 48, 64):
     _sweep(f"sweep-e{_e}", n_elts=_e, elts_per_layer=_e)
 for _k in (500, 2000):
     _sweep(f"sweep-k{_k}", k_min=_k, k_max=_k)

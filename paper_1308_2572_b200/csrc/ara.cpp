@@ -330,6 +330,10 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                                             &ctx->launches)
                     : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     }
+    if (e == cudaErrorInvalidValue && ctx->store.width == 24)  // only the pair scan reads W = 24
+        return fail(ctx, ARA_ERR_UNSUPPORTED,
+                    "24-column rows need the warp-batched schedule (ARA_SCAN_SCHED unset, "
+                    "<= 2^31 trials)");
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     if (ara::t_last_kernel) ctx->last_kernel = ara::t_last_kernel;
     return ARA_OK;
@@ -777,8 +781,6 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
             st.n_cols.push_back(elt_offsets[l + 1] - elt_offsets[l]);
             maxE = std::max(maxE, st.n_cols.back());
         }
-        const uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);
-        st.width = W;
         st.bits = ctx->bits;
         if (const char *g = getenv("ARA_SCAN_GROUP")) st.group_override = atoi(g);
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
@@ -786,6 +788,11 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *q = getenv("ARA_PAIR_SCAN")) st.pair_scan = atoi(q) != 0;
         st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
                                                        elt_index);
+        uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);
+        // 17-24 ELTs: 24-column rows for the 3-lane pair scan instead of padding to 32 (only
+        // that kernel reads them; the compare-select scan.cu serves W = 32)
+        if (W == 32 && maxE <= 24 && st.scaled && st.pair_scan) W = 24;
+        st.width = W;
         std::vector<uint32_t> map((size_t)C + 1, 0u);
         std::vector<uint32_t> uni;
         for (uint32_t c = elt_offsets[0]; c < elt_offsets[n_layers]; ++c) {

@@ -55,19 +55,21 @@ inline uint32_t row_width_for(uint32_t E)
 }
 
 // Column order inside a layer's W-element row segment.  W <= 16, and every fp32 store: logical
-// (column j at j).  fp64 stores of W >= 32 are LANE-INTERLEAVED: every kernel reading them runs
-// G = 4 lanes per trial, lane c owning the CH = W / 16 logical 32-byte chunks [CH c, CH c + CH)
-// (4 columns each, in ELT-sum order); physical chunk k G + c holds lane c's k-th chunk.  A group's
-// k-th 256-bit load instruction then reads one whole 128-byte line (4 lanes x 32 bytes) instead of
-// one sector in each of G lines: 1 L1 wavefront and 1 L2 request per line of the row instead of
-// G (W = 64: 4 instead of 16 per event; profiles/r2_tune_interleave.jsonl).
-__host__ __device__ inline bool row_interleaved(uint32_t W, int bits) { return bits == 64 && W >= 32; }
+// (column j at j).  fp64 stores of W >= 24 are LANE-INTERLEAVED: every kernel reading them runs
+// G lanes per trial (G = 3 for W = 24, 4 for W >= 32), lane c owning the CH = W / (4 G) logical
+// 32-byte chunks [CH c, CH c + CH) (4 columns each, in ELT-sum order); physical chunk k G + c
+// holds lane c's k-th chunk.  A group's k-th 256-bit load instruction then reads G contiguous
+// chunks (one whole 128-byte line for G = 4) instead of one sector in each of G lines: 1 L1
+// wavefront and 1 L2 request per line instead of G (W = 64: 4 instead of 16 per event;
+// profiles/r2_tune_interleave.jsonl).
+__host__ __device__ inline bool row_interleaved(uint32_t W, int bits) { return bits == 64 && W >= 24; }
 __host__ __device__ inline uint32_t row_phys_col(uint32_t j, uint32_t W, int bits)
 {
     if (!row_interleaved(W, bits)) return j;
-    const uint32_t ch = W / 16;                        // chunks per lane
+    const uint32_t g = W == 24 ? 3 : 4;                // lanes per trial
+    const uint32_t ch = W / (4 * g);                   // chunks per lane
     const uint32_t c = j / (4 * ch), k = (j / 4) % ch;  // owning lane, its chunk
-    return 4 * (k * 4 + c) + j % 4;
+    return 4 * (k * g + c) + j % 4;
 }
 
 // Decomposition for a store of width W; override (1, 2 or 4) selects G for W = 16 only.

@@ -73,11 +73,20 @@ struct TrialState {
 // One step of lane c on its row segment r: financial terms of its 8 columns, the ELT chain,
 // then (meaningful in lane G - 1) the occurrence and aggregate terms.  own is the lane's partial
 // of its own columns (the gather pin).  Returns inc8 (lane G - 1).
-template <int P, int X>
-__device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
-                                            uint32_t gmask, double &own, TrialState &st)
+// Chain hop: lane c > 0 receives lane c - 1's partial (src_up = its lane index; lane 0 its own).
+// Groups of 2 or 4 lanes use the segmented up-shuffle, 3-lane groups (10 per warp) an indexed one.
+template <int G>
+__device__ __forceinline__ double hop_up(uint32_t gmask, double v, uint32_t src_up)
 {
-    constexpr int G = 2 * P;
+    if constexpr (G == 2 || G == 4) return __shfl_up_sync(gmask, v, 1, G);
+    else return __shfl_sync(gmask, v, src_up);
+}
+
+template <int G, int X>
+__device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
+                                            uint32_t gmask, uint32_t src_up, uint32_t src_last,
+                                            double &own, TrialState &st)
+{
     double f[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -91,7 +100,7 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
     own = a;
 #pragma unroll
     for (int h = 1; h < G; ++h) {
-        double x = __shfl_up_sync(gmask, a, 1, G);
+        double x = hop_up<G>(gmask, a, src_up);
 #pragma unroll
         for (int j = 0; j < 8; ++j) x = radd(x, f[j]);
         a = x;
@@ -99,7 +108,7 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
     // lines 15-29 on lo2 = a (lane G - 1; with per-event increments (X == 2) every lane of the
     // group gets lane G - 1's lo and carries the same trial state, so that each lane can keep and
     // store its own share of the chunk's increments without shared memory)
-    if constexpr (X == 2) a = __shfl_sync(gmask, a, G - 1, G);
+    if constexpr (X == 2) a = __shfl_sync(gmask, a, src_last);
     const double t2 = rsub(a, T.occ_ret2);
     const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
     st.S4 = radd(st.S4, oc4);
@@ -112,16 +121,16 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
     return inc8;
 }
 
-// The lane's two 32-byte chunks: adjacent for P = 1; G chunks apart for P = 2, whose 32-column
-// rows are lane-interleaved (ara_internal.h row_phys_col), so that each of the two load
-// instructions of a group reads one whole line.
-template <int P>
+// The lane's two 32-byte chunks: adjacent for G = 2 (16 columns, one line); G chunks apart for
+// G = 3 and 4, whose 24- and 32-column rows are lane-interleaved (ara_internal.h row_phys_col),
+// so that each of the group's two load instructions reads G contiguous chunks.
+template <int G>
 __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
                                         uint32_t idx, Chunk<double> (&r)[2])
 {
     const double *p = my_rows + (size_t)idx * stride;
     load_row_chunk(p, r[0]);
-    load_row_chunk(p + (P == 1 ? 4 : 4 * 2 * P), r[1]);
+    load_row_chunk(p + (G == 2 ? 4 : 4 * G), r[1]);
 }
 
 // F4 increments of an aligned 8-event chunk: lane c of the group holds the increments of the
@@ -129,15 +138,19 @@ __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint
 // pair_step) and stores them as one 8 PER-byte segment -- the group writes the chunk's 64 bytes
 // contiguously, L2 evict-first (scan_common.cuh store_v4).
 template <int G>
-__device__ __forceinline__ void keep_inc(double (&slot)[8 / G], double inc8, int j, uint32_t c)
+constexpr int kIncPer = (8 + G - 1) / G;  // increments of a chunk held per lane
+template <int G>
+__device__ __forceinline__ void keep_inc(double (&slot)[kIncPer<G>], double inc8, int j,
+                                         uint32_t c)
 {
-    constexpr int PER = 8 / G;
+    constexpr int PER = kIncPer<G>;
     if (j / PER == (int)c) slot[j % PER] = inc8 * 0.125;
 }
 template <int G>
-__device__ __forceinline__ void store_inc(const double (&slot)[8 / G], double *dst, uint32_t c)
+__device__ __forceinline__ void store_inc(const double (&slot)[kIncPer<G>], double *dst,
+                                          uint32_t c)
 {
-    constexpr int PER = 8 / G;
+    constexpr int PER = kIncPer<G>;
     double *d = dst + c * PER;
     if constexpr (PER == 4) {
         if ((((uintptr_t)dst) & 63u) == 0) {
@@ -151,7 +164,8 @@ __device__ __forceinline__ void store_inc(const double (&slot)[8 / G], double *d
         }
     }
 #pragma unroll
-    for (int k = 0; k < PER; ++k) d[k] = slot[k];
+    for (int k = 0; k < PER; ++k)
+        if (c * PER + k < 8) d[k] = slot[k];
 }
 
 // Row index of the event at step J of the current 8-event chunk (J = 8, 9: the next chunk; past
@@ -165,7 +179,7 @@ __device__ __forceinline__ uint32_t chunk_row(int J, const uint32_t (&idc)[8],
     return more ? row_index<MM>(look, idn[J - 8 < 8 ? J - 8 : 0], bad) : look.zero_base;
 }
 
-template <int P, int MM, int X>
+template <int G, int MM, int X>
 __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
                                           const uint32_t *__restrict__ bitmap,
                                           const double *__restrict__ rows,
@@ -174,14 +188,16 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
-    constexpr int G = 2 * P;
-    constexpr uint32_t W = 16 * P;
+    constexpr uint32_t W = 8 * G;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;
     // group mask: the groups of a warp run different trials (ragged lengths, head/tail loops)
     const uint32_t gmask = (G == 32) ? kFull : (((1u << G) - 1u) << (lane - c));
     const bool writer = c == G - 1;
-    const uint32_t B = 32 / G, gw = lane / G;  // groups per warp, this group's index in it
+    // groups per warp, this group's index in it (G = 3: 10 groups, lanes 30 and 31 idle)
+    const uint32_t B = 32 / G, gw = lane / G;
+    const bool active = gw < B;
+    const uint32_t src_up = c ? lane - 1 : lane, src_last = lane - c + G - 1;
     const uint64_t warp_g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) / 32;
     const uint64_t n_tickets = s.n_trials * n_layers;
@@ -200,7 +216,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     // a warp takes B consecutive tickets at a time from the device counter.
     for (uint64_t ticket = warp_g * B + gw;;) {
         if (ticket - gw >= n_tickets) break;  // warp-uniform
-        if (ticket < n_tickets) {
+        if (active && ticket < n_tickets) {
             const uint64_t q = ticket / n_layers;
             const uint64_t t = s.perm ? (uint64_t)s.perm[q] : q;
             const uint32_t layer = (uint32_t)(ticket - q * n_layers);
@@ -216,7 +232,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 T.occ_lim4 = 4.0 * L.occ_lim;
                 T.agg_ret4 = 4.0 * L.agg_ret;
                 T.agg_lim8 = 8.0 * L.agg_lim;
-                my_rows = rows + (size_t)layer * W + (P == 1 ? 8 * c : 4 * c);
+                my_rows = rows + (size_t)layer * W + (G == 2 ? 8 * c : 4 * c);
                 ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
                 if (X) {
                     mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
@@ -236,8 +252,8 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             };
             auto single = [&](uint64_t e) {
                 Chunk<double> r[2];
-                gather2<P>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
-                out(pair_step<P, X>(r, T, gmask, own, st), e);
+                gather2<G>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
+                out(pair_step<G, X>(r, T, gmask, src_up, src_last, own, st), e);
             };
             uint64_t e = 0;
             // head: single events until the id pointer is 32-byte aligned
@@ -245,7 +261,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             // body: chunks of 8 events; the ids of chunk i + 1 are in flight during chunk i, the
             // gather of event j + 1 while event j is computed
             const uint64_t n_chunks = (k - e) / 8;
-            double slot[8 / G];  // X == 2: this lane's share of the chunk's increments
+            double slot[kIncPer<G>];  // X == 2: this lane's share of the chunk's increments
             auto out8 = [&](double inc8, int j) {  // body events: kept in registers
                 if constexpr (X == 2) keep_inc<G>(slot, inc8, j, c);
             };
@@ -254,7 +270,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 load_ids8(tr + e, id_c);
                 if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
                 Chunk<double> ra[2], rb[2];
-                gather2<P>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
+                gather2<G>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -262,11 +278,11 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
-                        gather2<P>(my_rows, row_stride, pin(ib, own), rb);
-                        out8(pair_step<P, X>(ra, T, gmask, own, st), j);
+                        gather2<G>(my_rows, row_stride, pin(ib, own), rb);
+                        out8(pair_step<G, X>(ra, T, gmask, src_up, src_last, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
-                        gather2<P>(my_rows, row_stride, pin(ic, own), ra);
-                        out8(pair_step<P, X>(rb, T, gmask, own, st), j + 1);
+                        gather2<G>(my_rows, row_stride, pin(ic, own), ra);
+                        out8(pair_step<G, X>(rb, T, gmask, src_up, src_last, own, st), j + 1);
                     }
                     if constexpr (X == 2)
                         if (inc_row) store_inc<G>(slot, inc_row + beg + e0, c);
@@ -299,7 +315,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     }
 }
 
-template <int P, int MINB, int MM, int X>
+template <int G, int MINB, int MM, int X>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     pair_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                      const uint32_t *__restrict__ bitmap, const double *__restrict__ rows,
@@ -307,18 +323,18 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
 {
     if constexpr (MM == 2) {
         if (!probe_use_bitmap(s.probe)) {
-            pair_body<P, 1, X>(s, map, bitmap, rows, terms, n_layers);
+            pair_body<G, 1, X>(s, map, bitmap, rows, terms, n_layers);
             return;
         }
     }
-    pair_body<P, MM, X>(s, map, bitmap, rows, terms, n_layers);
+    pair_body<G, MM, X>(s, map, bitmap, rows, terms, n_layers);
 }
 
-template <int P, int MINB, int MM, int X>
+template <int G, int MINB, int MM, int X>
 cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream)
 {
-    auto kern = pair_scan_kernel<P, MINB, MM, X>;
+    auto kern = pair_scan_kernel<G, MINB, MM, X>;
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
     static std::atomic<int> occ_cache[kMaxDevices];
     int occ = 0;
@@ -326,7 +342,7 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     if (e != cudaSuccess) return e;
     // One wave of resident blocks; the warp-batched tickets balance the work.  Fewer blocks when
     // the tickets cannot fill them.
-    constexpr uint64_t groups_per_block = kScanThreads / (2 * P);
+    constexpr uint64_t groups_per_block = (kScanThreads / 32) * (32 / G);
     const uint64_t n_tickets = s.n_trials * st.n_layers;
     uint64_t blocks = (uint64_t)sm_count * occ;
     const uint64_t need = (n_tickets + groups_per_block - 1) / groups_per_block;
@@ -335,7 +351,7 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
-    static const std::string name = kernel_name("pair_scan_kernel", P, MINB, MM, X);
+    static const std::string name = kernel_name("pair_scan_kernel", G, MINB, MM, X);
     t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),
@@ -343,28 +359,28 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     return cudaGetLastError();
 }
 
-template <int P, int MINB, int X>
+template <int G, int MINB, int X>
 cudaError_t launch_pair_mm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                            cudaStream_t stream)
 {
-    if (!st.d_rows_direct) return launch_pair<P, MINB, 0, X>(st, s, sm_count, stream);
+    if (!st.d_rows_direct) return launch_pair<G, MINB, 0, X>(st, s, sm_count, stream);
     if (st.map_mode == 1 || (X && st.map_mode == 2))
-        return launch_pair<P, MINB, 1, X>(st, s, sm_count, stream);
+        return launch_pair<G, MINB, 1, X>(st, s, sm_count, stream);
     if constexpr (X == 0)
-        if (st.map_mode == 2) return launch_pair<P, MINB, 2, 0>(st, s, sm_count, stream);
-    return launch_pair<P, MINB, 0, X>(st, s, sm_count, stream);
+        if (st.map_mode == 2) return launch_pair<G, MINB, 2, 0>(st, s, sm_count, stream);
+    return launch_pair<G, MINB, 0, X>(st, s, sm_count, stream);
 }
 
-template <int P, int MINB>
+template <int G, int MINB>
 cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                           cudaStream_t stream)
 {
 #ifndef ARA_F4_MINB
 #define ARA_F4_MINB MINB
 #endif
-    if (s.event_inc) return launch_pair_mm<P, ARA_F4_MINB, 2>(st, s, sm_count, stream);
-    if (s.max_occ) return launch_pair_mm<P, MINB, 1>(st, s, sm_count, stream);
-    return launch_pair_mm<P, MINB, 0>(st, s, sm_count, stream);
+    if (s.event_inc) return launch_pair_mm<G, ARA_F4_MINB, 2>(st, s, sm_count, stream);
+    if (s.max_occ) return launch_pair_mm<G, MINB, 1>(st, s, sm_count, stream);
+    return launch_pair_mm<G, MINB, 0>(st, s, sm_count, stream);
 }
 
 }  // namespace
@@ -374,7 +390,7 @@ bool pair_scan_eligible(const DeviceStore &st, const ScanLaunch &s)
     // W = 64: scan.cu's G = 4 lanes x 16 columns is faster (61.8 vs 72.7 ms for 1M x 1000,
     // profiles/r2_tune_pair.jsonl): 8 lanes x 8 columns issue twice the chain adds
     return st.bits == 64 && st.scaled && s.counter && s.done && st.pair_scan &&
-           (st.width == 16 || st.width == 32);
+           (st.width == 16 || st.width == 24 || st.width == 32);
 }
 
 cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
@@ -383,8 +399,9 @@ cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
     switch (st.width) {
-        case 16: return launch_pair_x<1, 3>(st, s, sm_count, stream);
-        case 32: return launch_pair_x<2, 3>(st, s, sm_count, stream);
+        case 16: return launch_pair_x<2, 3>(st, s, sm_count, stream);
+        case 24: return launch_pair_x<3, 3>(st, s, sm_count, stream);
+        case 32: return launch_pair_x<4, 3>(st, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
     }
 }

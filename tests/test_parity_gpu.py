@@ -77,7 +77,7 @@ def test_medium_shape_bit_identical(stream):
     assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds, n_threads=8))
 
 
-@pytest.mark.parametrize("n_elts", [1, 3, 4, 5, 8, 15, 16, 17, 32, 33, 64])
+@pytest.mark.parametrize("n_elts", [1, 3, 4, 5, 8, 15, 16, 17, 20, 24, 32, 33, 40, 48, 64])
 def test_elts_per_layer_widths(stream, n_elts):
     """Every row width class (W = 4..64; padded columns must be exactly neutral)."""
     spec = datagen.PRESETS["tiny"].replace(n_elts=n_elts, elts_per_layer=n_elts, n_trials=400,
@@ -761,7 +761,8 @@ def _sampled_oracle(spec, ds, sel):
 
 
 @pytest.mark.parametrize("preset,hoist", [
-    ("portfolio", False), ("sweep-e4", False), ("sweep-e64", False), ("sweep-k2000", False),
+    ("portfolio", False), ("sweep-e4", False), ("sweep-e20", False), ("sweep-e24", False),
+    ("sweep-e32", False), ("sweep-e48", False), ("sweep-e64", False), ("sweep-k2000", False),
     ("sweep-ragged", False), ("sweep-h10", False), ("sweep-n8m", False),
     ("sweep-bigstore", False),
     ("headline", True), ("portfolio", True), ("sweep-h10", True), ("sweep-bigstore", True)])
