@@ -786,6 +786,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *m = getenv("ARA_SCAN_MINB")) st.min_blocks = atoi(m);
         if (const char *d = getenv("ARA_SCAN_DEPTH")) st.depth = atoi(d);
         if (const char *q = getenv("ARA_PAIR_SCAN")) st.pair_scan = atoi(q) != 0;
+        if (const char *q = getenv("ARA_PAIR_WIDE")) st.pair_wide = atoi(q) != 0;
         st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
                                                        elt_index);
         uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);

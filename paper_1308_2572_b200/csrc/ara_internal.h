@@ -132,6 +132,7 @@ struct DeviceStore {
     // layer term is below 2^960, so the exactly scaled clamps cannot overflow
     bool scaled = false;
     bool pair_scan = true;       // tuning: ARA_PAIR_SCAN=0 runs scan.cu's kernel instead
+    bool pair_wide = true;       // tuning: ARA_PAIR_WIDE=0 keeps W = 48 / 64 on scan.cu
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     // Row addressing of the scan: 0 = through d_map (dense rows);
     // 1 = direct (rows indexed by catalogue id, no map read); 2 = direct behind a presence

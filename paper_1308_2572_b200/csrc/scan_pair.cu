@@ -42,26 +42,15 @@ using namespace scan_detail;
 
 constexpr unsigned kFull = 0xffffffffu;
 
+template <int N>
 struct ScaledTerms {
-    double rate[8], ret[8], lim2[8];  // this lane's columns
+    double rate[N], ret[N], lim2[N];  // this lane's N = 4 CH columns
     double occ_ret2, occ_lim4, agg_ret4, agg_lim8;
 };
 
 // 2 max(x, 0), exact (see the file comment)
 __device__ __forceinline__ double twice_max0(double x) { return __dadd_rn(x, fabs(x)); }
 
-// max(x, 0) on the integer pipe (sign mask; -0 -> +0): the columns j < ARA_PAIR_INTMAX compute
-// x2 = l (2 rate) - 2 ret = 2 x exactly (power-of-two scaled terms) and clear it when negative,
-// moving one fp64 operation per column to the ALU (tuning; default 0)
-#ifndef ARA_PAIR_INTMAX
-#define ARA_PAIR_INTMAX 0
-#endif
-__device__ __forceinline__ double int_max0(double x)
-{
-    const int hi = __double2hiint(x), lo = __double2loint(x);
-    const int keep = ~(hi >> 31);
-    return __hiloint2double(hi & keep, lo & keep);
-}
 __device__ __forceinline__ double cmin(double m, double lim) { return (lim < m) ? lim : m; }
 
 // Trial state of the group's last lane (lane G - 1 ends every step with the full ELT sum of its
@@ -82,27 +71,29 @@ __device__ __forceinline__ double hop_up(uint32_t gmask, double v, uint32_t src_
     else return __shfl_sync(gmask, v, src_up);
 }
 
-template <int G, int X>
-__device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const ScaledTerms &T,
-                                            uint32_t gmask, uint32_t src_up, uint32_t src_last,
-                                            double &own, TrialState &st)
+template <int G, int CH, int X>
+__device__ __forceinline__ double pair_step(const Chunk<double> (&r)[CH],
+                                            const ScaledTerms<4 * CH> &T, uint32_t gmask,
+                                            uint32_t src_up, uint32_t src_last, double &own,
+                                            TrialState &st)
 {
-    double f[8];
+    constexpr int N = 4 * CH;
+    double f[N];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < N; ++j) {
         const double x = rsub(rmul(r[j >> 2].v[j & 3], T.rate[j]), T.ret[j]);  // line 9
         f[j] = cmin(twice_max0(x), T.lim2[j]);
     }
     // lines 11-13: lane 0 starts at F2_0 (= 0 + F2_0), lane h continues lane h - 1's partial
     double a = f[0];
 #pragma unroll
-    for (int j = 1; j < 8; ++j) a = radd(a, f[j]);
+    for (int j = 1; j < N; ++j) a = radd(a, f[j]);
     own = a;
 #pragma unroll
     for (int h = 1; h < G; ++h) {
         double x = hop_up<G>(gmask, a, src_up);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x = radd(x, f[j]);
+        for (int j = 0; j < N; ++j) x = radd(x, f[j]);
         a = x;
     }
     // lines 15-29 on lo2 = a (lane G - 1; with per-event increments (X == 2) every lane of the
@@ -124,13 +115,13 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[2], const S
 // The lane's two 32-byte chunks: adjacent for G = 2 (16 columns, one line); G chunks apart for
 // G = 3 and 4, whose 24- and 32-column rows are lane-interleaved (ara_internal.h row_phys_col),
 // so that each of the group's two load instructions reads G contiguous chunks.
-template <int G>
+template <int G, int CH>
 __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
-                                        uint32_t idx, Chunk<double> (&r)[2])
+                                        uint32_t idx, Chunk<double> (&r)[CH])
 {
     const double *p = my_rows + (size_t)idx * stride;
-    load_row_chunk(p, r[0]);
-    load_row_chunk(p + (G == 2 ? 4 : 4 * G), r[1]);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) load_row_chunk(p + (G == 2 ? 4 : 4 * G) * k, r[k]);
 }
 
 // F4 increments of an aligned 8-event chunk: lane c of the group holds the increments of the
@@ -179,7 +170,7 @@ __device__ __forceinline__ uint32_t chunk_row(int J, const uint32_t (&idc)[8],
     return more ? row_index<MM>(look, idn[J - 8 < 8 ? J - 8 : 0], bad) : look.zero_base;
 }
 
-template <int G, int MM, int X>
+template <int G, int CH, int MM, int X>
 __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
                                           const uint32_t *__restrict__ bitmap,
                                           const double *__restrict__ rows,
@@ -188,7 +179,8 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 {
     extern __shared__ __align__(16) uint32_t sbits[];  // map mode 2 only
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
-    constexpr uint32_t W = 8 * G;
+    constexpr uint32_t W = 4 * G * CH;
+    constexpr int N = 4 * CH;  // columns per lane
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;
     // group mask: the groups of a warp run different trials (ragged lengths, head/tail loops)
@@ -206,7 +198,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     const RowLookup look{map, sbits, s.catalogue_size, zb, s.bitmap_log2};
     const uint64_t base = s.offsets[0];
 
-    ScaledTerms T;
+    ScaledTerms<N> T;
     const double *__restrict__ my_rows = rows;
     double *ylt_row = s.ylt, *mo_row = nullptr, *inc_row = nullptr;
     uint32_t cur_layer = 0xffffffffu;
@@ -223,16 +215,16 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             if (layer != cur_layer) {
                 const LayerTermsT<double> &L = terms[layer];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {  // int_max0 columns: doubled rate, retention
-                    T.rate[j] = (j < ARA_PAIR_INTMAX ? 2.0 : 1.0) * L.rate[8 * c + j];
-                    T.ret[j] = (j < ARA_PAIR_INTMAX ? 2.0 : 1.0) * L.ret[8 * c + j];
-                    T.lim2[j] = 2.0 * L.lim[8 * c + j];
+                for (int j = 0; j < N; ++j) {
+                    T.rate[j] = L.rate[N * c + j];
+                    T.ret[j] = L.ret[N * c + j];
+                    T.lim2[j] = 2.0 * L.lim[N * c + j];
                 }
                 T.occ_ret2 = 2.0 * L.occ_ret;
                 T.occ_lim4 = 4.0 * L.occ_lim;
                 T.agg_ret4 = 4.0 * L.agg_ret;
                 T.agg_lim8 = 8.0 * L.agg_lim;
-                my_rows = rows + (size_t)layer * W + (G == 2 ? 8 * c : 4 * c);
+                my_rows = rows + (size_t)layer * W + (G == 2 ? N * c : 4 * c);
                 ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
                 if (X) {
                     mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
@@ -251,9 +243,9 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                     if (inc_row && writer) inc_row[beg + e] = inc8 * 0.125;
             };
             auto single = [&](uint64_t e) {
-                Chunk<double> r[2];
-                gather2<G>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
-                out(pair_step<G, X>(r, T, gmask, src_up, src_last, own, st), e);
+                Chunk<double> r[CH];
+                gather2<G, CH>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
+                out(pair_step<G, CH, X>(r, T, gmask, src_up, src_last, own, st), e);
             };
             uint64_t e = 0;
             // head: single events until the id pointer is 32-byte aligned
@@ -269,8 +261,8 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 uint32_t id_c[8], id_n[8];
                 load_ids8(tr + e, id_c);
                 if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
-                Chunk<double> ra[2], rb[2];
-                gather2<G>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
+                Chunk<double> ra[CH], rb[CH];
+                gather2<G, CH>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -278,11 +270,11 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
-                        gather2<G>(my_rows, row_stride, pin(ib, own), rb);
-                        out8(pair_step<G, X>(ra, T, gmask, src_up, src_last, own, st), j);
+                        gather2<G, CH>(my_rows, row_stride, pin(ib, own), rb);
+                        out8(pair_step<G, CH, X>(ra, T, gmask, src_up, src_last, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
-                        gather2<G>(my_rows, row_stride, pin(ic, own), ra);
-                        out8(pair_step<G, X>(rb, T, gmask, src_up, src_last, own, st), j + 1);
+                        gather2<G, CH>(my_rows, row_stride, pin(ic, own), ra);
+                        out8(pair_step<G, CH, X>(rb, T, gmask, src_up, src_last, own, st), j + 1);
                     }
                     if constexpr (X == 2)
                         if (inc_row) store_inc<G>(slot, inc_row + beg + e0, c);
@@ -315,7 +307,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     }
 }
 
-template <int G, int MINB, int MM, int X>
+template <int G, int CH, int MINB, int MM, int X>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     pair_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                      const uint32_t *__restrict__ bitmap, const double *__restrict__ rows,
@@ -323,18 +315,18 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
 {
     if constexpr (MM == 2) {
         if (!probe_use_bitmap(s.probe)) {
-            pair_body<G, 1, X>(s, map, bitmap, rows, terms, n_layers);
+            pair_body<G, CH, 1, X>(s, map, bitmap, rows, terms, n_layers);
             return;
         }
     }
-    pair_body<G, MM, X>(s, map, bitmap, rows, terms, n_layers);
+    pair_body<G, CH, MM, X>(s, map, bitmap, rows, terms, n_layers);
 }
 
-template <int G, int MINB, int MM, int X>
+template <int G, int CH, int MINB, int MM, int X>
 cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream)
 {
-    auto kern = pair_scan_kernel<G, MINB, MM, X>;
+    auto kern = pair_scan_kernel<G, CH, MINB, MM, X>;
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
     static std::atomic<int> occ_cache[kMaxDevices];
     int occ = 0;
@@ -351,7 +343,7 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
-    static const std::string name = kernel_name("pair_scan_kernel", G, MINB, MM, X);
+    static const std::string name = kernel_name("pair_scan_kernel", G, CH, MINB, MM, X);
     t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),
@@ -359,38 +351,42 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     return cudaGetLastError();
 }
 
-template <int G, int MINB, int X>
+template <int G, int CH, int MINB, int X>
 cudaError_t launch_pair_mm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                            cudaStream_t stream)
 {
-    if (!st.d_rows_direct) return launch_pair<G, MINB, 0, X>(st, s, sm_count, stream);
+    if (!st.d_rows_direct) return launch_pair<G, CH, MINB, 0, X>(st, s, sm_count, stream);
     if (st.map_mode == 1 || (X && st.map_mode == 2))
-        return launch_pair<G, MINB, 1, X>(st, s, sm_count, stream);
+        return launch_pair<G, CH, MINB, 1, X>(st, s, sm_count, stream);
     if constexpr (X == 0)
-        if (st.map_mode == 2) return launch_pair<G, MINB, 2, 0>(st, s, sm_count, stream);
-    return launch_pair<G, MINB, 0, X>(st, s, sm_count, stream);
+        if (st.map_mode == 2) return launch_pair<G, CH, MINB, 2, 0>(st, s, sm_count, stream);
+    return launch_pair<G, CH, MINB, 0, X>(st, s, sm_count, stream);
 }
 
-template <int G, int MINB>
+template <int G, int CH, int MINB>
 cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                           cudaStream_t stream)
 {
 #ifndef ARA_F4_MINB
 #define ARA_F4_MINB MINB
 #endif
-    if (s.event_inc) return launch_pair_mm<G, ARA_F4_MINB, 2>(st, s, sm_count, stream);
-    if (s.max_occ) return launch_pair_mm<G, MINB, 1>(st, s, sm_count, stream);
-    return launch_pair_mm<G, MINB, 0>(st, s, sm_count, stream);
+    if (s.event_inc) return launch_pair_mm<G, CH, ARA_F4_MINB, 2>(st, s, sm_count, stream);
+    if (s.max_occ) return launch_pair_mm<G, CH, MINB, 1>(st, s, sm_count, stream);
+    return launch_pair_mm<G, CH, MINB, 0>(st, s, sm_count, stream);
 }
 
 }  // namespace
 
+#ifndef ARA_PAIR_WIDE_MINB
+#define ARA_PAIR_WIDE_MINB 2
+#endif
 bool pair_scan_eligible(const DeviceStore &st, const ScanLaunch &s)
 {
     // W = 64: scan.cu's G = 4 lanes x 16 columns is faster (61.8 vs 72.7 ms for 1M x 1000,
     // profiles/r2_tune_pair.jsonl): 8 lanes x 8 columns issue twice the chain adds
     return st.bits == 64 && st.scaled && s.counter && s.done && st.pair_scan &&
-           (st.width == 16 || st.width == 24 || st.width == 32);
+           (st.width == 16 || st.width == 24 || st.width == 32 ||
+            (st.pair_wide && (st.width == 48 || st.width == 64)));
 }
 
 cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count,
@@ -399,9 +395,11 @@ cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
     switch (st.width) {
-        case 16: return launch_pair_x<2, 3>(st, s, sm_count, stream);
-        case 24: return launch_pair_x<3, 3>(st, s, sm_count, stream);
-        case 32: return launch_pair_x<4, 3>(st, s, sm_count, stream);
+        case 16: return launch_pair_x<2, 2, 3>(st, s, sm_count, stream);
+        case 24: return launch_pair_x<3, 2, 3>(st, s, sm_count, stream);
+        case 32: return launch_pair_x<4, 2, 3>(st, s, sm_count, stream);
+        case 48: return launch_pair_x<4, 3, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
+        case 64: return launch_pair_x<4, 4, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
     }
 }
