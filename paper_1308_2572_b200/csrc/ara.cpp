@@ -330,10 +330,10 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
                                             &ctx->launches)
                     : ara::launch_scan(ctx->store, s, ctx->sm_count, ctx->stream, &ctx->launches);
     }
-    if (e == cudaErrorInvalidValue && ctx->store.width == 24)  // only the pair scan reads W = 24
-        return fail(ctx, ARA_ERR_UNSUPPORTED,
-                    "24-column rows need the warp-batched schedule (ARA_SCAN_SCHED unset, "
-                    "<= 2^31 trials)");
+    if (e == cudaErrorInvalidValue && (ctx->store.ilv == 2 || ctx->store.ilv == 3))
+        return fail(ctx, ARA_ERR_UNSUPPORTED,  // only the pair scan reads these row layouts
+                    "rows laid out for the pair scan need the warp-batched schedule "
+                    "(ARA_SCAN_SCHED unset, <= 2^31 trials)");
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scan kernel launch");
     if (ara::t_last_kernel) ctx->last_kernel = ara::t_last_kernel;
     return ARA_OK;
@@ -359,7 +359,7 @@ void build_rows(const ara_ctx *ctx, const ara::DeviceStore &st, const std::vecto
             const uint32_t j = elt_index[elt_offsets[l] + c];
             for (uint64_t r = ctx->rec_off[j]; r < ctx->rec_off[j + 1]; ++r)
                 rows[(size_t)map[ctx->rec_ids[r]] * stride + (size_t)l * W +
-                     ara::row_phys_col(c, W, st.bits)] = (R)ctx->rec_losses[r];
+                     ara::row_phys_col(c, W, st.ilv)] = (R)ctx->rec_losses[r];
             lt[l].rate[c] = (R)ctx->fin[j].rate;
             lt[l].ret[c] = (R)ctx->fin[j].retention;
             lt[l].lim[c] = (R)ctx->fin[j].limit;
@@ -787,6 +787,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *d = getenv("ARA_SCAN_DEPTH")) st.depth = atoi(d);
         if (const char *q = getenv("ARA_PAIR_SCAN")) st.pair_scan = atoi(q) != 0;
         if (const char *q = getenv("ARA_PAIR_WIDE")) st.pair_wide = atoi(q) != 0;
+        if (const char *q = getenv("ARA_PAIR_G2")) st.pair_g2 = atoi(q) != 0;
         st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
                                                        elt_index);
         uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);
@@ -794,6 +795,12 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         // that kernel reads them; the compare-select scan.cu serves W = 32)
         if (W == 32 && maxE <= 24 && st.scaled && st.pair_scan) W = 24;
         st.width = W;
+        // lanes per trial of the kernel that reads the rows (the interleave, ara_internal.h):
+        // W >= 32 four lanes (ARA_PAIR_G2=1, tuning: 25-32 ELTs on the 2-lane pair scan)
+        st.ilv = (ctx->bits != 64 || W <= 16) ? 0
+                 : W == 24                     ? 3
+                 : (W == 32 && st.scaled && st.pair_scan && st.pair_g2) ? 2
+                                               : 4;
         std::vector<uint32_t> map((size_t)C + 1, 0u);
         std::vector<uint32_t> uni;
         for (uint32_t c = elt_offsets[0]; c < elt_offsets[n_layers]; ++c) {
@@ -1195,7 +1202,7 @@ ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, doubl
             // logical column order (the device rows of W >= 32 are lane-interleaved)
             for (size_t u = 0; u <= st.n_union; ++u)
                 for (uint32_t j = 0; j < st.width; ++j) {
-                    const size_t i = u * st.width + ara::row_phys_col(j, st.width, st.bits);
+                    const size_t i = u * st.width + ara::row_phys_col(j, st.width, st.ilv);
                     h_rows[u * st.width + j] = st.bits == 32
                                                    ? (double)((const float *)tmp.data())[i]
                                                    : ((const double *)tmp.data())[i];

@@ -54,22 +54,21 @@ inline uint32_t row_width_for(uint32_t E)
     return 16 * ((nc + 3) / 4);       // multiples of 16 doubles
 }
 
-// Column order inside a layer's W-element row segment.  W <= 16, and every fp32 store: logical
-// (column j at j).  fp64 stores of W >= 24 are LANE-INTERLEAVED: every kernel reading them runs
-// G lanes per trial (G = 3 for W = 24, 4 for W >= 32), lane c owning the CH = W / (4 G) logical
-// 32-byte chunks [CH c, CH c + CH) (4 columns each, in ELT-sum order); physical chunk k G + c
-// holds lane c's k-th chunk.  A group's k-th 256-bit load instruction then reads G contiguous
-// chunks (one whole 128-byte line for G = 4) instead of one sector in each of G lines: 1 L1
-// wavefront and 1 L2 request per line instead of G (W = 64: 4 instead of 16 per event;
-// profiles/r2_tune_interleave.jsonl).
-__host__ __device__ inline bool row_interleaved(uint32_t W, int bits) { return bits == 64 && W >= 24; }
-__host__ __device__ inline uint32_t row_phys_col(uint32_t j, uint32_t W, int bits)
+// Column order inside a layer's W-element row segment (DeviceStore::ilv).  ilv = 0 (W <= 16, and
+// every fp32 store): logical, column j at j.  ilv = g > 0 (fp64 stores of W >= 24): LANE-
+// INTERLEAVED for the kernel that reads the store with g lanes per trial, lane c owning the
+// CH = W / (4 g) logical 32-byte chunks [CH c, CH c + CH) (4 columns each, in ELT-sum order):
+// physical chunk k g + c holds lane c's k-th chunk.  A group's k-th 256-bit load instruction then
+// reads g contiguous chunks (a whole 128-byte line for g = 4) instead of one sector in each of g
+// lines: 1 L1 wavefront and 1 L2 request per line instead of g (W = 64: 4 instead of 16 per
+// event; profiles/r2_tune_interleave.jsonl).  g = 3 for W = 24; for W = 32, 2 when the 2-lane
+// pair scan reads it, else 4; g = 4 for W = 48, 64.
+__host__ __device__ inline uint32_t row_phys_col(uint32_t j, uint32_t W, uint32_t ilv)
 {
-    if (!row_interleaved(W, bits)) return j;
-    const uint32_t g = W == 24 ? 3 : 4;                // lanes per trial
-    const uint32_t ch = W / (4 * g);                   // chunks per lane
+    if (ilv == 0) return j;
+    const uint32_t ch = W / (4 * ilv);                 // chunks per lane
     const uint32_t c = j / (4 * ch), k = (j / 4) % ch;  // owning lane, its chunk
-    return 4 * (k * g + c) + j % 4;
+    return 4 * (k * ilv + c) + j % 4;
 }
 
 // Decomposition for a store of width W; override (1, 2 or 4) selects G for W = 16 only.
@@ -133,6 +132,9 @@ struct DeviceStore {
     bool scaled = false;
     bool pair_scan = true;       // tuning: ARA_PAIR_SCAN=0 runs scan.cu's kernel instead
     bool pair_wide = true;       // tuning: ARA_PAIR_WIDE=0 keeps W = 48 / 64 on scan.cu
+    bool pair_g2 = false;        // tuning: ARA_PAIR_G2=1 runs W = 32 on 2 lanes x 16 columns
+                                 // (half the chain adds, but 255 registers: 29.3 vs 26.1 ms)
+    uint32_t ilv = 0;            // row layout: 0 logical, g = lane-interleaved for g lanes
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     // Row addressing of the scan: 0 = through d_map (dense rows);
     // 1 = direct (rows indexed by catalogue id, no map read); 2 = direct behind a presence

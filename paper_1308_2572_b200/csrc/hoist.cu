@@ -41,8 +41,8 @@ __global__ void __launch_bounds__(256) hoist_oc_kernel(const R *__restrict__ row
                                                        const LayerTermsT<R> *__restrict__ terms,
                                                        const uint32_t *__restrict__ union_ids,
                                                        uint32_t n_union, uint32_t n_layers,
-                                                       uint32_t W, uint32_t LP, int direct,
-                                                       R *__restrict__ oc)
+                                                       uint32_t W, uint32_t ilv, uint32_t LP,
+                                                       int direct, R *__restrict__ oc)
 {
     const uint64_t n = (uint64_t)n_union * n_layers;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) hoist_oc_kernel(const R *__restrict__ row
         const R *x = rows + (size_t)u * n_layers * W + (size_t)l * W;
         R lo = R(0);  // lines 11-13: ((0 + F_0) + F_1) + ..., padded columns add +0
         for (uint32_t j = 0; j < W; ++j) {
-            const R xj = x[row_phys_col(j, W, sizeof(R) == 8 ? 64 : 32)];
+            const R xj = x[row_phys_col(j, W, ilv)];
             const R f = dmin(dmax0(rsub(rmul(xj, T.rate[j]), T.ret[j])), T.lim[j]);  // line 9
             lo = radd(lo, f);
         }
@@ -307,11 +307,11 @@ cudaError_t launch_hoist_oc(const DeviceStore &st, cudaStream_t stream, uint64_t
     if (st.bits == 32)
         hoist_oc_kernel<float><<<blocks, 256, 0, stream>>>(
             (const float *)st.d_rows, (const LayerTermsT<float> *)st.d_terms, st.d_union_ids,
-            st.n_union, st.n_layers, st.width, st.oc_lp, st.oc_direct, (float *)st.d_oc);
+            st.n_union, st.n_layers, st.width, st.ilv, st.oc_lp, st.oc_direct, (float *)st.d_oc);
     else
         hoist_oc_kernel<double><<<blocks, 256, 0, stream>>>(
             (const double *)st.d_rows, (const LayerTermsT<double> *)st.d_terms, st.d_union_ids,
-            st.n_union, st.n_layers, st.width, st.oc_lp, st.oc_direct, (double *)st.d_oc);
+            st.n_union, st.n_layers, st.width, st.ilv, st.oc_lp, st.oc_direct, (double *)st.d_oc);
     return cudaGetLastError();
 }
 

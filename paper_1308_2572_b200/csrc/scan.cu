@@ -574,6 +574,8 @@ cudaError_t launch_scan(const DeviceStore &st, const ScanLaunch &s, int sm_count
                         cudaStream_t stream, uint64_t *launches)
 {
     if (s.n_trials == 0) return cudaSuccess;
+    // this kernel reads logical rows (W <= 16) or rows interleaved for its 4 lanes (W >= 32)
+    if (st.ilv != 0 && st.ilv != 4) return cudaErrorInvalidValue;
     ++*launches;
     if (s.perm && (s.max_occ || s.event_inc)) {  // F4 outputs, length-bucketed (fp64 store)
         if (st.bits != 64) { --*launches; return cudaErrorInvalidValue; }

@@ -115,13 +115,13 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[CH],
 // The lane's two 32-byte chunks: adjacent for G = 2 (16 columns, one line); G chunks apart for
 // G = 3 and 4, whose 24- and 32-column rows are lane-interleaved (ara_internal.h row_phys_col),
 // so that each of the group's two load instructions reads G contiguous chunks.
-template <int G, int CH>
+template <int G, int CH, bool ILV>
 __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
                                         uint32_t idx, Chunk<double> (&r)[CH])
 {
     const double *p = my_rows + (size_t)idx * stride;
 #pragma unroll
-    for (int k = 0; k < CH; ++k) load_row_chunk(p + (G == 2 ? 4 : 4 * G) * k, r[k]);
+    for (int k = 0; k < CH; ++k) load_row_chunk(p + (ILV ? 4 * G : 4) * k, r[k]);
 }
 
 // F4 increments of an aligned 8-event chunk: lane c of the group holds the increments of the
@@ -181,6 +181,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     load_bitmap<MM>(sbits, bitmap, s.bitmap_log2);
     constexpr uint32_t W = 4 * G * CH;
     constexpr int N = 4 * CH;  // columns per lane
+    constexpr bool ILV = W >= 24;  // lane-interleaved rows (ara_internal.h row_phys_col, ilv = G)
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t c = lane % G;
     // group mask: the groups of a warp run different trials (ragged lengths, head/tail loops)
@@ -224,7 +225,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 T.occ_lim4 = 4.0 * L.occ_lim;
                 T.agg_ret4 = 4.0 * L.agg_ret;
                 T.agg_lim8 = 8.0 * L.agg_lim;
-                my_rows = rows + (size_t)layer * W + (G == 2 ? N * c : 4 * c);
+                my_rows = rows + (size_t)layer * W + (ILV ? 4 * c : N * c);
                 ylt_row = s.ylt + (size_t)layer * s.ylt_ld;
                 if (X) {
                     mo_row = s.max_occ ? s.max_occ + (size_t)layer * s.max_occ_ld : nullptr;
@@ -244,7 +245,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             };
             auto single = [&](uint64_t e) {
                 Chunk<double> r[CH];
-                gather2<G, CH>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
+                gather2<G, CH, ILV>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
                 out(pair_step<G, CH, X>(r, T, gmask, src_up, src_last, own, st), e);
             };
             uint64_t e = 0;
@@ -262,7 +263,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 load_ids8(tr + e, id_c);
                 if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
                 Chunk<double> ra[CH], rb[CH];
-                gather2<G, CH>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
+                gather2<G, CH, ILV>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -270,10 +271,10 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
-                        gather2<G, CH>(my_rows, row_stride, pin(ib, own), rb);
+                        gather2<G, CH, ILV>(my_rows, row_stride, pin(ib, own), rb);
                         out8(pair_step<G, CH, X>(ra, T, gmask, src_up, src_last, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
-                        gather2<G, CH>(my_rows, row_stride, pin(ic, own), ra);
+                        gather2<G, CH, ILV>(my_rows, row_stride, pin(ic, own), ra);
                         out8(pair_step<G, CH, X>(rb, T, gmask, src_up, src_last, own, st), j + 1);
                     }
                     if constexpr (X == 2)
@@ -397,7 +398,9 @@ cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_
     switch (st.width) {
         case 16: return launch_pair_x<2, 2, 3>(st, s, sm_count, stream);
         case 24: return launch_pair_x<3, 2, 3>(st, s, sm_count, stream);
-        case 32: return launch_pair_x<4, 2, 3>(st, s, sm_count, stream);
+        case 32:
+            if (st.ilv == 2) return launch_pair_x<2, 4, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
+            return launch_pair_x<4, 2, 3>(st, s, sm_count, stream);
         case 48: return launch_pair_x<4, 3, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
         case 64: return launch_pair_x<4, 4, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
