@@ -78,7 +78,7 @@ def test_full_size_every_entry_twice(config):
         torch.cuda.synchronize()
     # 16 ELTs, every event in the store (h = 1): the second run launches the plain row-by-id
     # instantiation of the pair scan (the kernel bench.py times)
-    assert kernels[1] == "pair_scan_kernel<1, 3, 1, 0>", kernels
+    assert kernels[1] == "pair_scan_kernel<2, 2, 3, 1, 0>", kernels
     ctx.close()
 
 
@@ -126,7 +126,7 @@ def test_adversarial_pair_scan(n_elts):
         ctx.ara_run(to_dev(ds.trial_offsets, "u64"), to_dev(ds.events, "u32"), ylt,
                     flags=ara.ARA_RUN_SYNC)
         check_every_entry(ylt.cpu().numpy(), oracle.run_analysis(ds))
-        assert ctx.ara_get_info().last_kernel.decode().startswith("pair_scan_kernel<1,")
+        assert ctx.ara_get_info().last_kernel.decode().startswith("pair_scan_kernel<2, 2,")
         ctx.close()
 
 

@@ -3,7 +3,8 @@
 
     compute-sanitizer --tool memcheck python tools/sanitize_cases.py
 
-single layer (map modes 0-2), multi-layer per-layer rows, union rows with the shared F row and
+single layer (map modes 0-2), the pair scans of every row width (16-64 columns),
+multi-layer per-layer rows, union rows with the shared F row and
 with register shuffles, F4 outputs, fp32, host-buffer run, PML/TVaR, the hoisted scan, and the
 runs that follow the previous run's length / hit-probe verdicts (identity order, mode-1 body).  Each YLT is checked against
 the oracle (test infrastructure), so a run that passes under the sanitizer is also correct."""
@@ -73,6 +74,12 @@ def main():
         run(datagen.generate(tiny), env=[("ARA_MAP_MODE", mode)])
     run(datagen.generate(tiny), outputs=True)
     run(datagen.generate(tiny), precision=32)
+    # pair scans of every row width (W = 16 / 24 / 32 / 48 / 64: 2-4 lanes, interleaved rows),
+    # plain and with F4 outputs, ragged lengths
+    for e in (16, 20, 32, 40, 64):
+        wide = tiny.replace(n_elts=e, elts_per_layer=e, k_min=0, k_max=30, seed=11 + e)
+        run(datagen.generate(wide))
+        run(datagen.generate(wide), outputs=True)
     pf = datagen.PRESETS["portfolio"].replace(n_trials=200, k_min=0, k_max=60,
                                               catalogue_size=100_000, pool_size=2000,
                                               records_per_elt=1000)
