@@ -74,7 +74,7 @@ __device__ __forceinline__ double hop_up(uint32_t gmask, double v, uint32_t src_
 template <int G, int CH, int X>
 __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[CH],
                                             const ScaledTerms<4 * CH> &T, uint32_t gmask,
-                                            uint32_t src_up, uint32_t src_last, double &own,
+                                            uint32_t src_up, double &own,
                                             TrialState &st)
 {
     constexpr int N = 4 * CH;
@@ -96,10 +96,7 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[CH],
         for (int j = 0; j < N; ++j) x = radd(x, f[j]);
         a = x;
     }
-    // lines 15-29 on lo2 = a (lane G - 1; with per-event increments (X == 2) every lane of the
-    // group gets lane G - 1's lo and carries the same trial state, so that each lane can keep and
-    // store its own share of the chunk's increments without shared memory)
-    if constexpr (X == 2) a = __shfl_sync(gmask, a, src_last);
+    // lines 15-29 on lo2 = a (lane G - 1)
     const double t2 = rsub(a, T.occ_ret2);
     const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
     st.S4 = radd(st.S4, oc4);
@@ -124,39 +121,19 @@ __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint
     for (int k = 0; k < CH; ++k) load_row_chunk(p + (ILV ? 4 * G : 4) * k, r[k]);
 }
 
-// F4 increments of an aligned 8-event chunk: lane c of the group holds the increments of the
-// chunk's events [c PER, c PER + PER) in registers (every lane computes every increment, see
-// pair_step) and stores them as one 8 PER-byte segment -- the group writes the chunk's 64 bytes
-// contiguously, L2 evict-first (scan_common.cuh store_v4).
-template <int G>
-constexpr int kIncPer = (8 + G - 1) / G;  // increments of a chunk held per lane
-template <int G>
-__device__ __forceinline__ void keep_inc(double (&slot)[kIncPer<G>], double inc8, int j,
-                                         uint32_t c)
+// F4 increments of an aligned 8-event chunk: the last lane (the one that carries the trial
+// state) keeps each half chunk's 4 increments in registers and stores them as one 32-byte
+// segment, L2 evict-first (scan_common.cuh store_v4): no shared memory, no warp barriers, no
+// extra shuffles (profiles/r2_tune_interleave.jsonl: 15.4 ms with round 1's shared-memory
+// staging, 14.7 ms with a broadcast of lo to the group and one 64-byte store per group, 13.6 ms).
+__device__ __forceinline__ void store_inc4(double *d, const double (&slot)[4])
 {
-    constexpr int PER = kIncPer<G>;
-    if (j / PER == (int)c) slot[j % PER] = inc8 * 0.125;
-}
-template <int G>
-__device__ __forceinline__ void store_inc(const double (&slot)[kIncPer<G>], double *dst,
-                                          uint32_t c)
-{
-    constexpr int PER = kIncPer<G>;
-    double *d = dst + c * PER;
-    if constexpr (PER == 4) {
-        if ((((uintptr_t)dst) & 63u) == 0) {
-            store_v4(d, slot[0], slot[1], slot[2], slot[3]);
-            return;
-        }
-    } else if constexpr (PER == 2) {
-        if ((((uintptr_t)dst) & 63u) == 0) {
-            store_v2(d, slot[0], slot[1]);
-            return;
-        }
-    }
+    if ((((uintptr_t)d) & 31u) == 0) {
+        store_v4(d, slot[0], slot[1], slot[2], slot[3]);
+    } else {
 #pragma unroll
-    for (int k = 0; k < PER; ++k)
-        if (c * PER + k < 8) d[k] = slot[k];
+        for (int q = 0; q < 4; ++q) d[q] = slot[q];
+    }
 }
 
 // Row index of the event at step J of the current 8-event chunk (J = 8, 9: the next chunk; past
@@ -190,7 +167,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     // groups per warp, this group's index in it (G = 3: 10 groups, lanes 30 and 31 idle)
     const uint32_t B = 32 / G, gw = lane / G;
     const bool active = gw < B;
-    const uint32_t src_up = c ? lane - 1 : lane, src_last = lane - c + G - 1;
+    const uint32_t src_up = c ? lane - 1 : lane;
     const uint64_t warp_g = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) / 32;
     const uint64_t n_tickets = s.n_trials * n_layers;
@@ -246,7 +223,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             auto single = [&](uint64_t e) {
                 Chunk<double> r[CH];
                 gather2<G, CH, ILV>(my_rows, row_stride, row_index<MM>(look, load_id(tr + e), bad), r);
-                out(pair_step<G, CH, X>(r, T, gmask, src_up, src_last, own, st), e);
+                out(pair_step<G, CH, X>(r, T, gmask, src_up, own, st), e);
             };
             uint64_t e = 0;
             // head: single events until the id pointer is 32-byte aligned
@@ -254,9 +231,13 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             // body: chunks of 8 events; the ids of chunk i + 1 are in flight during chunk i, the
             // gather of event j + 1 while event j is computed
             const uint64_t n_chunks = (k - e) / 8;
-            double slot[kIncPer<G>];  // X == 2: this lane's share of the chunk's increments
+            double slot[4];    // X == 2: the writer lane's increments of half a chunk
+            uint64_t e0w = 0;  // YET position of the current chunk
             auto out8 = [&](double inc8, int j) {  // body events: kept in registers
-                if constexpr (X == 2) keep_inc<G>(slot, inc8, j, c);
+                if constexpr (X == 2) {
+                    slot[j & 3] = inc8 * 0.125;  // meaningful in the writer lane
+                    if ((j & 3) == 3 && inc_row && writer) store_inc4(inc_row + beg + e0w + (j - 3), slot);
+                }
             };
             if (n_chunks) {
                 uint32_t id_c[8], id_n[8];
@@ -268,17 +249,16 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
                     const uint64_t e0 = e + 8 * i;
+                    e0w = e0;
 #pragma unroll
                     for (int j = 0; j < 8; j += 2) {
                         const uint32_t ib = chunk_row<MM>(j + 1, id_c, id_n, more, look, bad);
                         gather2<G, CH, ILV>(my_rows, row_stride, pin(ib, own), rb);
-                        out8(pair_step<G, CH, X>(ra, T, gmask, src_up, src_last, own, st), j);
+                        out8(pair_step<G, CH, X>(ra, T, gmask, src_up, own, st), j);
                         const uint32_t ic = chunk_row<MM>(j + 2, id_c, id_n, more, look, bad);
                         gather2<G, CH, ILV>(my_rows, row_stride, pin(ic, own), ra);
-                        out8(pair_step<G, CH, X>(rb, T, gmask, src_up, src_last, own, st), j + 1);
+                        out8(pair_step<G, CH, X>(rb, T, gmask, src_up, own, st), j + 1);
                     }
-                    if constexpr (X == 2)
-                        if (inc_row) store_inc<G>(slot, inc_row + beg + e0, c);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
                     if (i + 2 < n_chunks) load_ids8(tr + e + 8 * (i + 2), id_n);
