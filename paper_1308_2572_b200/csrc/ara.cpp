@@ -264,7 +264,10 @@ ara_status launch_layers(ara_ctx *ctx, uint64_t n, const uint64_t *d_off, const 
     const bool balance = ctx->sched == 0 && (!extra || ctx->store.bits == 64) &&
                          n <= 0x7fffffffull;  // u32 permutation, CUB's int item count
     const bool sorted = balance && !ctx->lengths_equal;
-    const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1);
+    // (rows laid out for the 3-lane pair scan -- 17-24 ELTs -- are read by no other kernel: its
+    // warp-batched tickets whatever the trial count)
+    const bool dyn = balance || ctx->sched == 2 || (ctx->sched == 0 && ctx->store.n_layers == 1) ||
+                     (ctx->sched != 1 && (ctx->store.ilv == 2 || ctx->store.ilv == 3));
     const uint32_t *perm = nullptr;
     if (sorted) {
         cudaError_t e = ara::launch_length_sort(d_off, n, ctx->sort, ctx->sm_count, ctx->stream,
@@ -793,13 +796,13 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);
         // 17-24 ELTs: 24-column rows for the 3-lane pair scan instead of padding to 32 (only
         // that kernel reads them; the compare-select scan.cu serves W = 32)
-        if (W == 32 && maxE <= 24 && st.scaled && st.pair_scan) W = 24;
+        if (W == 32 && maxE <= 24 && st.scaled && st.pair_scan && ctx->sched != 1) W = 24;
         st.width = W;
         // lanes per trial of the kernel that reads the rows (the interleave, ara_internal.h):
         // W >= 32 four lanes (ARA_PAIR_G2=1, tuning: 25-32 ELTs on the 2-lane pair scan)
         st.ilv = (ctx->bits != 64 || W <= 16) ? 0
                  : W == 24                     ? 3
-                 : (W == 32 && st.scaled && st.pair_scan && st.pair_g2) ? 2
+                 : (W == 32 && st.scaled && st.pair_scan && st.pair_g2 && ctx->sched != 1) ? 2
                                                : 4;
         std::vector<uint32_t> map((size_t)C + 1, 0u);
         std::vector<uint32_t> uni;

@@ -395,16 +395,20 @@ def test_hoisted_scan_limits(stream):
 
 
 # --------------------------------------------------------------------------- store (A1)
-@pytest.mark.parametrize("preset", ["tiny", "medium"])
+@pytest.mark.parametrize("preset", ["tiny", "medium", "sweep-e20", "sweep-e32", "sweep-e48",
+                                    "sweep-e64"])
 def test_store_round_trip(stream, preset):
     """rows[map[e]][c] == DAT_c[e] for every catalogue id e and layer ELT c,
-    bit for bit; map[0] = 0 and row 0 is zero."""
+    bit for bit; map[0] = 0 and row 0 is zero.  The exported rows are in logical column order
+    also where the device rows are lane-interleaved (W >= 24)."""
     ds = datagen.generate(datagen.PRESETS[preset], with_yet=False)
     ctx = make_ctx(ds, stream)
     m, rows = ctx.ara_export_store(0, ds.catalogue_size)
     E = int(ds.elt_offsets[1])
     U, W = ctx.ara_layer_store_shape(0)
-    assert W == (E + 3) // 4 * 4 and m[0] == 0 and (rows[0] == 0).all()
+    # row widths: whole 32-byte chunks up to 8 ELTs, then 16, 24 (17-24 ELTs), 32, 48, 64
+    want_w = (E + 3) // 4 * 4 if E <= 8 else next(w for w in (16, 24, 32, 48, 64) if w >= E)
+    assert W == want_w and m[0] == 0 and (rows[0] == 0).all()
     assert (rows[:, E:] == 0).all()
     for c in range(E):
         j = int(ds.elt_index[c])
@@ -412,6 +416,26 @@ def test_store_round_trip(stream, preset):
         dat = oracle.build_dat(ds.catalogue_size, ds.rec_event_ids[a:b], ds.rec_losses[a:b])
         assert np.array_equal(rows[m, c].view(np.uint64), dat.view(np.uint64))
     assert U == len(np.unique(ds.rec_event_ids))
+    ctx.close()
+
+
+@pytest.mark.parametrize("sched", ["", "static", "dynamic"])
+def test_w24_rows_every_schedule(stream, monkeypatch, sched):
+    """17-24 ELTs: 24-column rows on the 3-lane pair scan under the default and dynamic
+    schedules (ARA_SCAN_SCHED=static keeps 32-column rows on the compare-select kernel); the YLT
+    is the oracle's either way, ragged and empty trials included."""
+    if sched:
+        monkeypatch.setenv("ARA_SCAN_SCHED", sched)
+    spec = datagen.PRESETS["tiny"].replace(n_elts=20, elts_per_layer=20, n_trials=700, k_min=0,
+                                           k_max=45, seed=24)
+    ds = datagen.generate(spec)
+    ctx = make_ctx(ds, stream)
+    got = gpu_ylt(ds, stream, ctx=ctx)
+    assert_bit_identical(got, oracle.run_analysis(ds))
+    _, W = ctx.ara_layer_store_shape(0)
+    kern = ctx.ara_get_info().last_kernel.decode()
+    assert (W, kern.startswith("pair_scan_kernel<3,")) == ((32, False) if sched == "static"
+                                                           else (24, True)), (W, kern)
     ctx.close()
 
 
