@@ -327,7 +327,9 @@ typedef struct {
     int layer_kernel;            /* how several layers are scanned: 0 = rows
                                     per layer (one fused launch); 1 = union rows, layer sums
                                     through a shared-memory F row; 2 = union rows, layer sums
-                                    through register shuffles.  Identical results.          */
+                                    through register shuffles; 3 = union rows, half of each
+                                    layer's ELTs in its own lane (blocks of 8), the other half
+                                    by shuffles.  Identical results.                        */
     uint32_t gather_row_bytes;   /* row bytes the scan gathers per event (all layers; the
                                     union row when layer_kernel > 0)                        */
     char last_kernel[64];        /* the scan-kernel instantiation the last ara_run* launched,

@@ -453,13 +453,54 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
         }
     }
     if (GU != 8) shfl = false;  // shuffle variants are built for GU = 8 only (portfolio.cu)
-    if (const char *e = getenv("ARA_PORTFOLIO_SHFL"))
+    // Block layout (portfolio.cu SH = 3): every layer has 16 ELTs, its first 8 (in layer order)
+    // form a block no other layer starts with, its last 8 another layer's first block or a block
+    // of its own, and the blocks partition J.  Lane l then holds layer l's first block in
+    // registers 0-7 (no shuffle for half the positions) and the second half comes from one
+    // source lane (configuration P: lane l + 1).  blk_lane[col] / blk_reg[col] place the columns.
+    std::vector<int> blk_lane(J.size(), -1), blk_reg(J.size(), -1);
+    std::vector<uint32_t> src2(L, 0);
+    bool blocks = GU == 8;
+    {
+        int n_blocks = 0;
+        auto place = [&](uint32_t l, uint32_t from, int lane) -> bool {  // 8 ELTs -> lane
+            for (uint32_t i = 0; i < 8; ++i) {
+                const int col = col_of[elt_index[elt_offsets[l] + from + i]];
+                if (blk_lane[col] >= 0) return false;
+                blk_lane[col] = lane;
+                blk_reg[col] = (int)i;
+            }
+            return true;
+        };
+        for (uint32_t l = 0; l < L && blocks; ++l)
+            blocks = st.n_cols[l] == (uint32_t)ara::kUnionMaxE && place(l, 0, (int)l);
+        n_blocks = (int)L;
+        for (uint32_t l = 0; l < L && blocks; ++l) {
+            const int c0 = col_of[elt_index[elt_offsets[l] + 8]];
+            int lane = blk_lane[c0];
+            if (lane >= 0) {  // an existing block: the same 8 ELTs in the same order
+                for (uint32_t i = 0; i < 8 && blocks; ++i) {
+                    const int col = col_of[elt_index[elt_offsets[l] + 8 + i]];
+                    blocks = blk_lane[col] == lane && blk_reg[col] == (int)i;
+                }
+            } else {
+                lane = n_blocks++;
+                blocks = lane < (int)GU && place(l, 8, lane);
+            }
+            src2[l] = (uint32_t)lane;
+        }
+        for (size_t col = 0; col < J.size() && blocks; ++col) blocks = blk_lane[col] >= 0;
+    }
+    if (const char *e = getenv("ARA_PORTFOLIO_SHFL")) {
         if (atoi(e) == 0) shfl = false;
+        if (atoi(e) == 0 || atoi(e) == 2) blocks = false;  // 2: the per-position shuffles (tuning)
+    }
     // the union column that holds J[col]: lane c's registers 0-3 are columns 4c..4c+3 and
     // registers 4-7 are columns 4(c+GU)..4(c+GU)+3 (portfolio.cu, the two gathers of a group)
     auto ucol = [&](uint32_t col) -> uint32_t {
-        if (!shfl) return col;
-        const uint32_t r = (uint32_t)reg_of[col], c = (uint32_t)lane_of[col];
+        if (!shfl && !blocks) return col;
+        const uint32_t r = (uint32_t)(blocks ? blk_reg[col] : reg_of[col]);
+        const uint32_t c = (uint32_t)(blocks ? blk_lane[col] : lane_of[col]);
         return r < 4 ? 4 * c + r : 4 * (c + GU) + (r - 4);
     };
     std::vector<double> rows((size_t)(st.n_union + 1 + ara::kZeroRows) * WU, 0.0);
@@ -482,7 +523,7 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     for (uint32_t l = 0; l < L; ++l) {
         ut.n_cols[l] = st.n_cols[l];
         full16 = full16 && st.n_cols[l] == (uint32_t)ara::kUnionMaxE;
-        for (uint32_t i = 0; shfl && i < st.n_cols[l]; ++i) {
+        for (uint32_t i = 0; shfl && !blocks && i < st.n_cols[l]; ++i) {
             const uint32_t lane = (uint32_t)lane_of[col_of[elt_index[elt_offsets[l] + i]]];
             ut.src5[l][i / 6] |= lane << (5 * (i % 6));
         }
@@ -502,7 +543,8 @@ ara_status build_union(ara_ctx *ctx, const std::vector<uint32_t> &map,
     }
     ara::UnionStore &us = st.uni;
     us.GU = GU;
-    us.shfl = shfl ? (full16 ? 2 : 1) : 0;
+    for (uint32_t l = 0; l < L; ++l) ut.src2[l] = src2[l];
+    us.shfl = blocks ? 3 : shfl ? (full16 ? 2 : 1) : 0;
     us.scaled = st.scaled && st.pair_scan;  // ARA_PAIR_SCAN=0 also keeps the compare-selects
     us.n_cols = (uint32_t)J.size();
     us.zero_base = st.n_union + 1;
@@ -1166,7 +1208,7 @@ ara_status ara_get_info(const ara_ctx *ctx, ara_info *out)
     out->sm_count = ctx->sm_count;
     out->row_addressing = ctx->have_layers ? ctx->store.map_mode : 0;
     out->layer_kernel = !ctx->have_layers || !ctx->store.uni.enabled ? 0
-                        : 1 + (ctx->store.uni.shfl != 0);
+                        : ctx->store.uni.shfl == 3 ? 3 : 1 + (ctx->store.uni.shfl != 0);
     out->gather_row_bytes = !ctx->have_layers ? 0
                             : ctx->store.uni.enabled
                                 ? 8 * 8 * ctx->store.uni.GU

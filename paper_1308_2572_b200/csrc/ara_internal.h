@@ -99,6 +99,9 @@ struct UnionTermsDev {
     // in register i mod 8 of lane src(l, i) of the group; src5 packs the 16 source lanes of a
     // layer as 5-bit fields, six per word
     uint32_t src5[kUnionMaxLayers][3];
+    // block layout (shfl == 3): layer l's positions 0-7 are registers 0-7 of lane l, positions
+    // 8-15 registers 0-7 of lane src2[l]
+    uint32_t src2[kUnionMaxLayers];
     uint32_t n_cols[kUnionMaxLayers];    // ELTs of each layer
 };
 struct UnionStore {
@@ -108,7 +111,8 @@ struct UnionStore {
     uint32_t zero_base_direct = 0;       // C + 1: zero-row block of d_rows_direct
     uint32_t GU = 0;         // lanes per trial (2, 4 or 8); union row width WU = 8 * GU doubles
     int shfl = 0;            // layer sums: 0 = shared-memory F row; 1 = register shuffles
-                             // (general); 2 = register shuffles, every layer has 16 ELTs
+                             // (general); 2 = register shuffles, every layer has 16 ELTs;
+                             // 3 = blocks: half of every layer in its own lane's registers
     uint32_t n_cols = 0;     // |J|
     bool scaled = false;     // DeviceStore::scaled (the scaled-clamp instantiation may run)
     double *d_rows = nullptr;            // [(U+1+kZeroRows) * WU]

@@ -17,6 +17,12 @@
 // sequence, and carries layer l's running state.  Padding entries of a layer's column list point
 // at a zero slot (+0 is exactly neutral, reading R12).
 //
+// Block variant (SH = 3): when every layer is two blocks of 8 ELTs and the blocks partition J
+// (configuration P: layer l = block l then block l + 1), lane l holds layer l's first block in
+// its registers 0-7 and the second comes from one lane by 8 shuffles: half the shuffles of SH = 2
+// (the shuffles were the L1 data pipe's largest consumer: 8 wavefronts per trial-event against 4
+// for the union row).
+//
 // Register-shuffle variant (SH = 1, 2; UnionStore::shfl): when every ELT takes positions of one
 // residue mod 8 in all layers that hold it (configuration P), ara_set_layers places the ELT of
 // residue r in register r of some lane, so position i of EVERY layer is register i mod 8 of a
@@ -102,7 +108,8 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
     // register-shuffle layout: source lane of each position (5-bit fields; shfl uses bits 4:0)
     uint32_t src5[3] = {0, 0, 0};
     uint32_t my_n = 0;
-    if constexpr (SH != 0) {
+    const uint32_t src2 = SH == 3 ? ut->src2[ly] : 0;
+    if constexpr (SH == 1 || SH == 2) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) src5[i] = ut->src5[ly][i];
         my_n = has_layer ? ut->n_cols[ly] : 0;
@@ -140,6 +147,13 @@ __device__ __forceinline__ void portfolio_body(const ScanLaunch &s,
                 const uint32_t sl = (slot2[i >> 1] >> (16 * (i & 1))) & 0xffffu;
                 lo = radd(lo, myF[sl]);
             }
+        } else if constexpr (SH == 3) {
+            // block layout: positions 0-7 are this lane's own registers, positions 8-15
+            // registers 0-7 of lane src2 -- 8 shuffles per event instead of 16
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lo = radd(lo, f[i]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lo = radd(lo, __shfl_sync(gmask, f[i], src2, GU));
         } else {
             // position i of every layer lives in register i mod 8 (of lane src(l, i)): one
             // 64-bit shuffle per position serves all layers of the group, no shared memory
@@ -327,6 +341,13 @@ cudaError_t launch_pu(const UnionStore &us, const uint32_t *d_map, int map_mode,
                       cudaStream_t stream)
 {
     if constexpr (GU == 8) {
+        if (us.shfl == 3) {  // block layout (configuration P), scaled clamps when allowed
+            if constexpr (BAL)
+                if (us.scaled)
+                    return launch_pus<GU, BAL, 3, 1>(us, d_map, map_mode, d_bitmap, s, sm_count,
+                                                     stream);
+            return launch_pus<GU, BAL, 3, 0>(us, d_map, map_mode, d_bitmap, s, sm_count, stream);
+        }
         if (us.shfl == 2) {  // configuration P: the scaled clamps when the inputs allow them
             if constexpr (BAL)
                 if (us.scaled)

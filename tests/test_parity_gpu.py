@@ -279,7 +279,7 @@ def _portfolio_variant(kind):
     spec = datagen.PRESETS["portfolio"].replace(n_trials=700, k_min=0, k_max=90, seed=17)
     ds = datagen.generate(spec)
     if kind == "P":
-        return ds, 2
+        return ds, 3
     rng = np.random.default_rng(3)
     members = []
     for l in range(8):
@@ -295,18 +295,21 @@ def _portfolio_variant(kind):
 
 
 @pytest.mark.parametrize("kind", ["P", "ragged", "mixed"])
-@pytest.mark.parametrize("shfl_env", [None, "0"])
+@pytest.mark.parametrize("shfl_env", [None, "0", "2"])
 def test_portfolio_layer_sum_variants(stream, monkeypatch, kind, shfl_env):
-    """The union-row kernel's two ways of forming each layer's ordered ELT sum -- register
-    shuffles (when every ELT has one register residue across the layers that hold it) and the
-    shared-memory F row (always possible; forced with ARA_PORTFOLIO_SHFL=0) -- both give the
-    oracle's YLT bit for bit, including layers shorter than 16 ELTs (+0 padding)."""
+    """The union-row kernel's ways of forming each layer's ordered ELT sum -- blocks of 8 ELTs
+    in the layer's own lane plus 8 shuffles (configuration P), register shuffles per position
+    (when every ELT has one register residue across the layers that hold it; forced for P with
+    ARA_PORTFOLIO_SHFL=2) and the shared-memory F row (always possible; forced with
+    ARA_PORTFOLIO_SHFL=0) -- all give the oracle's YLT bit for bit, including layers shorter than
+    16 ELTs (+0 padding)."""
     if shfl_env is not None:
         monkeypatch.setenv("ARA_PORTFOLIO_SHFL", shfl_env)
     ds, expect = _portfolio_variant(kind)
     want = oracle.run_analysis(ds, n_threads=8)
     ctx = make_ctx(types_ns(ds), stream)
-    assert ctx.ara_get_info().layer_kernel == (1 if shfl_env == "0" else expect)
+    want_kernel = 1 if shfl_env == "0" else (2 if shfl_env == "2" and expect == 3 else expect)
+    assert ctx.ara_get_info().layer_kernel == want_kernel
     assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx), want)
     assert_bit_identical(gpu_ylt(types_ns(ds), stream, ctx=ctx, flags=ara.ARA_RUN_SYNC), want)
     ctx.close()

@@ -83,7 +83,8 @@ def main():
     pf = datagen.PRESETS["portfolio"].replace(n_trials=200, k_min=0, k_max=60,
                                               catalogue_size=100_000, pool_size=2000,
                                               records_per_elt=1000)
-    assert run(datagen.generate(pf)).layer_kernel == 2
+    assert run(datagen.generate(pf)).layer_kernel == 3
+    assert run(datagen.generate(pf), env=[("ARA_PORTFOLIO_SHFL", "2")]).layer_kernel == 2
     assert run(datagen.generate(pf), env=[("ARA_PORTFOLIO_SHFL", "0")]).layer_kernel == 1
     assert run(datagen.generate(pf), env=[("ARA_PORTFOLIO", "0")]).layer_kernel == 0
     run(datagen.generate(pf), outputs=True)
