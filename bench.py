@@ -95,22 +95,17 @@ def gather_ceiling():
     return best, src
 
 
-def lib_sha16():
-    import hashlib
-    from paper_1308_2572_b200 import ara
-    with open(ara.LIB_PATH, "rb") as f:
-        return hashlib.sha256(f.read()).hexdigest()[:16]
-
-
 def ncu_entry(kernel: str, config: str):
-    """The committed ncu counters (profiles/scan_traffic.json) of THIS kernel instantiation in
-    THIS libara.so build and config, else None (stale counters are never reported)."""
+    """The committed ncu counters (profiles/scan_traffic.json) of THIS kernel instantiation built
+    from THESE sources (paper_1308_2572_b200.build.source_sha16) and config, else None (stale
+    counters are never reported)."""
+    from paper_1308_2572_b200.build import source_sha16
     path = os.path.join(ROOT, "profiles", "scan_traffic.json")
     try:
         j = json.load(open(path))
     except Exception:
         return None
-    e = j.get(f"{kernel}|{lib_sha16()}|{config}")
+    e = j.get(f"{kernel}|{source_sha16()}|{config}")
     return e if isinstance(e, dict) else None
 
 
@@ -143,7 +138,7 @@ def roofline(args, spec, ctx, info, n_ev: int, n_loc: int, scan_ms: float) -> di
                                         "lts_throughput", "fp64_pipe", "alu_pipe",
                                         "issue_active", "warps_per_sm", "bound") if k in ent}
         physical["source"] = "profiles/scan_traffic.json (ncu --set full of this kernel " \
-                             "instantiation in this libara.so build)"
+                             "instantiation built from these sources)"
     if args.hoist:
         # the hoisted pass: one L1/L2 read of the per-event table per (occurrence, layer)
         U = ctx.ara_layer_store_shape(0)[0]

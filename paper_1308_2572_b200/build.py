@@ -40,6 +40,22 @@ def _sources():
     return [os.path.join(CSRC, f) for f in PER_FILE]
 
 
+def source_sha16() -> str:
+    """Hash of everything that determines libara.so's machine code: the kernel and host sources,
+    the internal headers, the public header and this script (flags).  nvcc output is not
+    byte-reproducible, so committed ncu counters are keyed by this instead of the binary."""
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(CSRC, "*")) + [os.path.join(INCLUDE, "ara.h"),
+                                                          os.path.abspath(__file__)])
+    for f in files:
+        if os.path.isfile(f) and not f.endswith((".o", ".so")):
+            h.update(os.path.basename(f).encode())
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True

@@ -3,17 +3,16 @@
 `ncu --set full` capture of a scan or portfolio launch.
 
     python tools/ncu_traffic.py CONFIG REPORT.ncu-rep N_TRIALS "bound text" [--source TEXT]
-                                [--lib paper_1308_2572_b200/libara.so]
 
 Reads the report's raw page (ncu -i ... --page raw --csv) and stores DRAM bytes per launch
 (dram__bytes_read.sum + dram__bytes_write.sum), L1 data-pipe / L1->L2 request / L2 / fp64 / ALU /
-issue utilisation and the duration under ncu, keyed "<kernel instantiation>|<sha256[:16] of the
-libara.so that ran>|<config>": bench.py reports an entry only for the same kernel of the same
-build, so a changed kernel never shows stale counters.  Run it on the report of the library
-that is committed alongside (the .so is rebuilt from the committed sources).
+issue utilisation and the duration under ncu, keyed "<kernel instantiation>|<source hash>|
+<config>" (paper_1308_2572_b200.build.source_sha16: the sources that determine libara.so's
+code; nvcc output itself is not byte-reproducible): bench.py reports an entry only for the same
+kernel built from the same sources, so a changed kernel never shows stale counters.  Run it on
+a report of the library built from the committed sources.
 """
 import csv
-import hashlib
 import io
 import re
 import json
@@ -48,15 +47,15 @@ def pct(d, key):
 def main():
     cfg, report, n_trials, bound = sys.argv[1:5]
     src = sys.argv[sys.argv.index("--source") + 1] if "--source" in sys.argv else report
-    lib = sys.argv[sys.argv.index("--lib") + 1] if "--lib" in sys.argv else os.path.join(
-        ROOT, "paper_1308_2572_b200", "libara.so")
-    sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
+    sys.path.insert(0, ROOT)
+    from paper_1308_2572_b200.build import source_sha16
+    sha = source_sha16()  # nvcc output is not byte-reproducible: key by the sources
     d = raw(report)
     m = re.search(r"(\w+<[^()]*>)\(", d["Kernel Name"][0])
     kern = m.group(1) if m else d["Kernel Name"][0]
     entry = {
         "kernel": kern,
-        "lib_sha16": sha,
+        "src_sha16": sha,
         "n_trials": int(n_trials),
         "dram_bytes_per_launch": num(d, "dram__bytes_read.sum") + num(d, "dram__bytes_write.sum"),
         "l2_to_l1_bytes": num(d, "l1tex__m_xbar2l1tex_read_bytes.sum"),
