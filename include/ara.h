@@ -148,8 +148,11 @@ ara_status ara_load_elts(ara_ctx *ctx, uint32_t catalogue_size, uint32_t n_elts,
  *   map[0..C]  (u32)  catalogue id -> dense row, 0 = event in none of the layer's ELTs
  *   rows[0..U][W]     fp64, row r = the losses of the r-th event of the union U of the layer's
  *                     ELT events, column j = the layer's j-th ELT (0 where absent); row 0 zero;
- *                     W = |E_l| rounded up to whole 32-byte chunks: 4, 8 or a multiple of
- *                     16 doubles (row_width_for in csrc/ara_internal.h)
+ *                     W = |E_l| rounded up to whole 32-byte chunks: 4, 8, 16, 24 (17-24
+ *                     ELTs on the 3-lane pair scan), 32, 48 or 64 doubles (row_width_for in
+ *                     csrc/ara_internal.h); on the device the columns of W >= 24 rows are
+ *                     lane-interleaved for the kernel that reads them (row_phys_col), exported
+ *                     in this logical order by ara_export_store
  * i.e. the paper's direct access tables (L124) re-laid-out event-major and compacted.
  *   n_layers               >= 1
  *   terms[n_layers]        layer terms T
@@ -333,7 +336,7 @@ typedef struct {
     uint32_t gather_row_bytes;   /* row bytes the scan gathers per event (all layers; the
                                     union row when layer_kernel > 0)                        */
     char last_kernel[64];        /* the scan-kernel instantiation the last ara_run* launched,
-                                    as ncu names it (e.g. "pair_scan_kernel<1, 3, 1, 0>");
+                                    as ncu names it (e.g. "pair_scan_kernel<2, 2, 3, 1, 0>");
                                     "" before the first run                                 */
 } ara_info;
 
@@ -344,7 +347,8 @@ ara_status ara_layer_store_shape(const ara_ctx *ctx, uint32_t layer, uint32_t *n
                                  uint32_t *row_width);
 
 /* Copy a layer's device store back to the host (store round-trip tests):
- * h_map[C+1] (u32) and h_rows[(U+1) * W] (fp64).  Either pointer may be NULL.  Synchronous. */
+ * h_map[C+1] (u32) and h_rows[(U+1) * W] (fp64, logical column order: column j = the layer's
+ * j-th ELT).  Either pointer may be NULL.  Synchronous. */
 ara_status ara_export_store(ara_ctx *ctx, uint32_t layer, uint32_t *h_map, double *h_rows);
 
 #ifdef __cplusplus
