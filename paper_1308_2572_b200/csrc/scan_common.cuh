@@ -23,12 +23,9 @@ struct Chunk {
     R v[N];
 };
 
-#ifndef ARA_ROWS_L2
-#define ARA_ROWS_L2 ""
-#endif
 __device__ __forceinline__ void load_row_chunk(const double *p, Chunk<double> &r)
 {
-    asm("ld.global.nc.L1::no_allocate" ARA_ROWS_L2 ".v4.f64 {%0,%1,%2,%3}, [%4];"
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
         : "l"(p));
 }

@@ -348,10 +348,7 @@ template <int G, int CH, int MINB>
 cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                           cudaStream_t stream)
 {
-#ifndef ARA_F4_MINB
-#define ARA_F4_MINB MINB
-#endif
-    if (s.event_inc) return launch_pair_mm<G, CH, ARA_F4_MINB, 2>(st, s, sm_count, stream);
+    if (s.event_inc) return launch_pair_mm<G, CH, MINB, 2>(st, s, sm_count, stream);
     if (s.max_occ) return launch_pair_mm<G, CH, MINB, 1>(st, s, sm_count, stream);
     return launch_pair_mm<G, CH, MINB, 0>(st, s, sm_count, stream);
 }
