@@ -666,7 +666,8 @@ def main():
                        "parallelism": f"trial-sharded x{world}, {args.scaling} scaling "
                                       + ("(PML/TVaR by sharded radix select, histograms "
                                          "all-reduced per pass)" if args.metrics == "sharded"
-                                         else "(NCCL all-gather of the YLT for PML/TVaR)")
+                                         else f"({dist.get_backend().upper()} all-gather of "
+                                              "the YLT for PML/TVaR)")
                        if world > 1 else "1 GPU",
                        "l2": l2_note(info, spec),
                        "return_periods": list(RETURN_PERIODS)},
