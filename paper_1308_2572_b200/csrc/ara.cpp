@@ -833,6 +833,7 @@ ara_status ara_set_layers(ara_ctx *ctx, uint32_t n_layers, const ara_layer_terms
         if (const char *q = getenv("ARA_PAIR_SCAN")) st.pair_scan = atoi(q) != 0;
         if (const char *q = getenv("ARA_PAIR_WIDE")) st.pair_wide = atoi(q) != 0;
         if (const char *q = getenv("ARA_PAIR_G2")) st.pair_g2 = atoi(q) != 0;
+        if (const char *q = getenv("ARA_PAIR_EV2")) st.pair_ev2 = atoi(q) != 0;
         st.scaled = ctx->bits == 64 && scaled_terms_ok(ctx, n_layers, terms, elt_offsets,
                                                        elt_index);
         uint32_t W = ctx->bits == 32 ? ara::row_width_for_f32(maxE) : ara::row_width_for(maxE);

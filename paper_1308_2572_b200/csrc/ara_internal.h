@@ -138,6 +138,7 @@ struct DeviceStore {
     bool pair_wide = true;       // tuning: ARA_PAIR_WIDE=0 keeps W = 48 / 64 on scan.cu
     bool pair_g2 = false;        // tuning: ARA_PAIR_G2=1 runs W = 32 on 2 lanes x 16 columns
                                  // (half the chain adds, but 255 registers: 29.3 vs 26.1 ms)
+    bool pair_ev2 = true;        // W = 32 / 48 plain scan: two events per step (ARA_PAIR_EV2=0: one)
     uint32_t ilv = 0;            // row layout: 0 logical, g = lane-interleaved for g lanes
     uint32_t *d_map = nullptr;   // [C+1] catalogue id -> row (0 = absent)
     // Row addressing of the scan: 0 = through d_map (dense rows);

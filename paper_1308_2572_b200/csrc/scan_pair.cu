@@ -42,6 +42,7 @@ using namespace scan_detail;
 
 constexpr unsigned kFull = 0xffffffffu;
 
+
 template <int N>
 struct ScaledTerms {
     double rate[N], ret[N], lim2[N];  // this lane's N = 4 CH columns
@@ -109,6 +110,62 @@ __device__ __forceinline__ double pair_step(const Chunk<double> (&r)[CH],
     return inc8;
 }
 
+// Two events of the trial at once (EV = 2): their ELT sums are independent, so the two chains
+// (and their hops) interleave and hide each other's add latency; lines 15-29 then run for the
+// first event and the second, in YET order.  Same operations, same order per event as pair_step.
+template <int G, int CH, int X>
+__device__ __forceinline__ void pair_step2(const Chunk<double> (&r0)[CH],
+                                           const Chunk<double> (&r1)[CH],
+                                           const ScaledTerms<4 * CH> &T, uint32_t gmask,
+                                           uint32_t src_up, double &own0, double &own1,
+                                           TrialState &st, double &inc0, double &inc1)
+{
+    constexpr int N = 4 * CH;
+    double f0[N], f1[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double x0 = rsub(rmul(r0[j >> 2].v[j & 3], T.rate[j]), T.ret[j]);  // line 9
+        const double x1 = rsub(rmul(r1[j >> 2].v[j & 3], T.rate[j]), T.ret[j]);
+        f0[j] = cmin(twice_max0(x0), T.lim2[j]);
+        f1[j] = cmin(twice_max0(x1), T.lim2[j]);
+    }
+    double a0 = f0[0], a1 = f1[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) {
+        a0 = radd(a0, f0[j]);
+        a1 = radd(a1, f1[j]);
+    }
+    own0 = a0;
+    own1 = a1;
+#pragma unroll
+    for (int h = 1; h < G; ++h) {
+        double x0 = hop_up<G>(gmask, a0, src_up);
+        double x1 = hop_up<G>(gmask, a1, src_up);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            x0 = radd(x0, f0[j]);
+            x1 = radd(x1, f1[j]);
+        }
+        a0 = x0;
+        a1 = x1;
+    }
+    double lo2[2] = {a0, a1}, inc[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {  // lines 15-29, first event first
+        const double t2 = rsub(lo2[e], T.occ_ret2);
+        const double oc4 = cmin(twice_max0(t2), T.occ_lim4);
+        st.S4 = radd(st.S4, oc4);
+        const double u4 = rsub(st.S4, T.agg_ret4);
+        const double C8 = cmin(twice_max0(u4), T.agg_lim8);
+        inc[e] = rsub(C8, st.C8);
+        st.lr8 = radd(st.lr8, inc[e]);
+        st.C8 = C8;
+        st.max4 = (st.max4 < oc4) ? oc4 : st.max4;
+    }
+    inc0 = inc[0];
+    inc1 = inc[1];
+}
+
 // The lane's two 32-byte chunks: adjacent for G = 2 (16 columns, one line); G chunks apart for
 // G = 3 and 4, whose 24- and 32-column rows are lane-interleaved (ara_internal.h row_phys_col),
 // so that each of the group's two load instructions reads G contiguous chunks.
@@ -147,7 +204,7 @@ __device__ __forceinline__ uint32_t chunk_row(int J, const uint32_t (&idc)[8],
     return more ? row_index<MM>(look, idn[J - 8 < 8 ? J - 8 : 0], bad) : look.zero_base;
 }
 
-template <int G, int CH, int MM, int X>
+template <int G, int CH, int MM, int X, int EV>
 __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *__restrict__ map,
                                           const uint32_t *__restrict__ bitmap,
                                           const double *__restrict__ rows,
@@ -245,6 +302,34 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
                 if (n_chunks > 1) load_ids8(tr + e + 8, id_n);
                 Chunk<double> ra[CH], rb[CH];
                 gather2<G, CH, ILV>(my_rows, row_stride, chunk_row<MM>(0, id_c, id_n, true, look, bad), ra);
+                if constexpr (EV == 2) {
+                    // two events per step: (ra, ra1) computed while (rb, rb1) load
+                    Chunk<double> ra1[CH], rb1[CH];
+                    double own1 = 0.0;
+                    gather2<G, CH, ILV>(my_rows, row_stride, chunk_row<MM>(1, id_c, id_n, true, look, bad), ra1);
+#pragma unroll 1
+                    for (uint64_t i = 0; i < n_chunks; ++i) {
+                        const bool more = i + 1 < n_chunks;
+                        e0w = e + 8 * i;
+#pragma unroll
+                        for (int j = 0; j < 8; j += 4) {
+                            double i0, i1;
+                            gather2<G, CH, ILV>(my_rows, row_stride, pin(chunk_row<MM>(j + 2, id_c, id_n, more, look, bad), own), rb);
+                            gather2<G, CH, ILV>(my_rows, row_stride, pin(chunk_row<MM>(j + 3, id_c, id_n, more, look, bad), own1), rb1);
+                            pair_step2<G, CH, X>(ra, ra1, T, gmask, src_up, own, own1, st, i0, i1);
+                            out8(i0, j);
+                            out8(i1, j + 1);
+                            gather2<G, CH, ILV>(my_rows, row_stride, pin(chunk_row<MM>(j + 4, id_c, id_n, more, look, bad), own), ra);
+                            gather2<G, CH, ILV>(my_rows, row_stride, pin(chunk_row<MM>(j + 5, id_c, id_n, more, look, bad), own1), ra1);
+                            pair_step2<G, CH, X>(rb, rb1, T, gmask, src_up, own, own1, st, i0, i1);
+                            out8(i0, j + 2);
+                            out8(i1, j + 3);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
+                        if (i + 2 < n_chunks) load_ids8(tr + e + 8 * (i + 2), id_n);
+                    }
+                } else {
 #pragma unroll 1
                 for (uint64_t i = 0; i < n_chunks; ++i) {
                     const bool more = i + 1 < n_chunks;
@@ -262,6 +347,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
 #pragma unroll
                     for (int j = 0; j < 8; ++j) id_c[j] = id_n[j];
                     if (i + 2 < n_chunks) load_ids8(tr + e + 8 * (i + 2), id_n);
+                }
                 }
                 e += 8 * n_chunks;
             }
@@ -288,7 +374,7 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
     }
 }
 
-template <int G, int CH, int MINB, int MM, int X>
+template <int G, int CH, int MINB, int MM, int X, int EV>
 __global__ void __launch_bounds__(kScanThreads, MINB)
     pair_scan_kernel(const ScanLaunch s, const uint32_t *__restrict__ map,
                      const uint32_t *__restrict__ bitmap, const double *__restrict__ rows,
@@ -296,18 +382,18 @@ __global__ void __launch_bounds__(kScanThreads, MINB)
 {
     if constexpr (MM == 2) {
         if (!probe_use_bitmap(s.probe)) {
-            pair_body<G, CH, 1, X>(s, map, bitmap, rows, terms, n_layers);
+            pair_body<G, CH, 1, X, EV>(s, map, bitmap, rows, terms, n_layers);
             return;
         }
     }
-    pair_body<G, CH, MM, X>(s, map, bitmap, rows, terms, n_layers);
+    pair_body<G, CH, MM, X, EV>(s, map, bitmap, rows, terms, n_layers);
 }
 
-template <int G, int CH, int MINB, int MM, int X>
+template <int G, int CH, int MINB, int MM, int X, int EV = 1>
 cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                         cudaStream_t stream)
 {
-    auto kern = pair_scan_kernel<G, CH, MINB, MM, X>;
+    auto kern = pair_scan_kernel<G, CH, MINB, MM, X, EV>;
     const size_t smem = MM == 2 ? bitmap_bytes(kBitmapLog2Scan) : 0;
     static std::atomic<int> occ_cache[kMaxDevices];
     int occ = 0;
@@ -324,7 +410,9 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
-    static const std::string name = kernel_name("pair_scan_kernel", G, CH, MINB, MM, X);
+    static const std::string name =
+        EV == 1 ? kernel_name("pair_scan_kernel", G, CH, MINB, MM, X)
+                : kernel_name("pair_scan_kernel", G, CH, MINB, MM, X, EV);
     t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),
@@ -332,29 +420,37 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     return cudaGetLastError();
 }
 
-template <int G, int CH, int MINB, int X>
+template <int G, int CH, int MINB, int X, int EV = 1>
 cudaError_t launch_pair_mm(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                            cudaStream_t stream)
 {
-    if (!st.d_rows_direct) return launch_pair<G, CH, MINB, 0, X>(st, s, sm_count, stream);
+    if (!st.d_rows_direct) return launch_pair<G, CH, MINB, 0, X, EV>(st, s, sm_count, stream);
     if (st.map_mode == 1 || (X && st.map_mode == 2))
-        return launch_pair<G, CH, MINB, 1, X>(st, s, sm_count, stream);
+        return launch_pair<G, CH, MINB, 1, X, EV>(st, s, sm_count, stream);
     if constexpr (X == 0)
-        if (st.map_mode == 2) return launch_pair<G, CH, MINB, 2, 0>(st, s, sm_count, stream);
-    return launch_pair<G, CH, MINB, 0, X>(st, s, sm_count, stream);
+        if (st.map_mode == 2) return launch_pair<G, CH, MINB, 2, 0, EV>(st, s, sm_count, stream);
+    return launch_pair<G, CH, MINB, 0, X, EV>(st, s, sm_count, stream);
 }
 
-template <int G, int CH, int MINB>
+// EV2MINB > 0: the plain scan (no F4 outputs) runs two events per step with that MINB
+// (ARA_PAIR_EV2=0 keeps one event per step)
+template <int G, int CH, int MINB, int EV2MINB = 0, int INCMINB = MINB>
 cudaError_t launch_pair_x(const DeviceStore &st, const ScanLaunch &s, int sm_count,
                           cudaStream_t stream)
 {
-    if (s.event_inc) return launch_pair_mm<G, CH, MINB, 2>(st, s, sm_count, stream);
+    if (s.event_inc) return launch_pair_mm<G, CH, INCMINB, 2>(st, s, sm_count, stream);
     if (s.max_occ) return launch_pair_mm<G, CH, MINB, 1>(st, s, sm_count, stream);
+    if constexpr (EV2MINB > 0)  // (not behind the presence bitmap: map mode 2 spills there)
+        if (st.pair_ev2 && !(st.d_rows_direct && st.map_mode == 2))
+            return launch_pair_mm<G, CH, EV2MINB, 0, 2>(st, s, sm_count, stream);
     return launch_pair_mm<G, CH, MINB, 0>(st, s, sm_count, stream);
 }
 
 }  // namespace
 
+#ifndef ARA_PAIR_INC_MINB16
+#define ARA_PAIR_INC_MINB16 3
+#endif
 #ifndef ARA_PAIR_WIDE_MINB
 #define ARA_PAIR_WIDE_MINB 2
 #endif
@@ -373,12 +469,12 @@ cudaError_t launch_pair_scan(const DeviceStore &st, const ScanLaunch &s, int sm_
     if (s.n_trials == 0) return cudaSuccess;
     ++*launches;
     switch (st.width) {
-        case 16: return launch_pair_x<2, 2, 3>(st, s, sm_count, stream);
+        case 16: return launch_pair_x<2, 2, 3, 0, ARA_PAIR_INC_MINB16>(st, s, sm_count, stream);
         case 24: return launch_pair_x<3, 2, 3>(st, s, sm_count, stream);
         case 32:
             if (st.ilv == 2) return launch_pair_x<2, 4, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
-            return launch_pair_x<4, 2, 3>(st, s, sm_count, stream);
-        case 48: return launch_pair_x<4, 3, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
+            return launch_pair_x<4, 2, 3, 3>(st, s, sm_count, stream);
+        case 48: return launch_pair_x<4, 3, ARA_PAIR_WIDE_MINB, 2>(st, s, sm_count, stream);
         case 64: return launch_pair_x<4, 4, ARA_PAIR_WIDE_MINB>(st, s, sm_count, stream);
         default: --*launches; return cudaErrorInvalidValue;
     }
