@@ -12,6 +12,13 @@
 // step needs only two hops -- computed fewer adds but ran 1.4-1.6x slower: its gathers were
 // scheduled too late under register pressure; profiles/r2_tune_pair.jsonl.)
 //
+// Two events per step (EV = 2; the plain scan of 25-48 ELTs, ARA_PAIR_EV2=0 turns it off): the
+// ELT sums of events j and j + 1 are independent, so pair_step2 runs both chains (and both hops)
+// interleaved and then lines 15-29 for j and j + 1 in order -- the wide rows are bound by the
+// latency of their serial chains (ncu: `wait` stalls first), and two chains per group hide half
+// of it (E = 32: 26.1 -> 24.5 ms, E = 48: 36.9 -> 35.0 ms at 1M x 1000; W = 16 and 24 are
+// faster with one event per step, W = 64 spills; profiles/r2_tune_ev2.jsonl).
+//
 // Exactly scaled clamps.  sm_100a has no fp64 min/max instruction; max(x, 0) as a compare-select
 // costs DSETP + 2 FSEL.  Instead the kernel carries power-of-two multiples of the oracle's values:
 //   2 max(x, 0) = x + |x|  exactly (x > 0: 2x is exact; x <= 0: x + |x| = +0 under RN),
@@ -410,9 +417,7 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
-    static const std::string name =
-        EV == 1 ? kernel_name("pair_scan_kernel", G, CH, MINB, MM, X)
-                : kernel_name("pair_scan_kernel", G, CH, MINB, MM, X, EV);
+    static const std::string name = kernel_name("pair_scan_kernel", G, CH, MINB, MM, X, EV);
     t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
         sl, st.d_map, st.d_bitmap, (const double *)(MM ? st.d_rows_direct : st.d_rows),

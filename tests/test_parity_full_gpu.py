@@ -78,7 +78,7 @@ def test_full_size_every_entry_twice(config):
         torch.cuda.synchronize()
     # 16 ELTs, every event in the store (h = 1): the second run launches the plain row-by-id
     # instantiation of the pair scan (the kernel bench.py times)
-    assert kernels[1] == "pair_scan_kernel<2, 2, 3, 1, 0>", kernels
+    assert kernels[1] == "pair_scan_kernel<2, 2, 3, 1, 0, 1>", kernels
     ctx.close()
 
 
