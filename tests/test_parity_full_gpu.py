@@ -204,6 +204,25 @@ def test_two_ranks_sharded_path():
     assert p["pass"] and p["ylt_mismatches"] == 0 and p["ylt_n"] == 100_000 and p["pml_exact"]
 
 
+def test_nccl_collectives_single_rank():
+    """dist.py's NCCL branches, which no multi-GPU box has run yet: one rank under torchrun with
+    an NCCL process group on this GPU (NCCL refuses two ranks on one device) broadcasts the
+    inputs, scans its slice through libara, all-gathers the YLT (all_gather_into_tensor) and
+    computes PML/TVaR both from the gathered row and by the all-reduced sharded radix select;
+    every YLT entry and PML equal the oracle's, TVaR within 1e-9 (tests/_nccl_rank.py)."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+         "--master-addr", "127.0.0.1", "--master-port", "29563",
+         os.path.join(ROOT, "tests", "_nccl_rank.py")],
+        capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    d = json.loads(lines[-1])
+    assert d["backend"] == "nccl" and d["world"] == 1
+    assert d["20000"]["mismatches"] == 0 and d["20001"]["mismatches"] == 0
+
+
 def test_oep_curve_from_max_occ():
     """F4 OEP: the exceedance curve of the per-trial maximum occurrence losses (ara_run_outputs
     max_occ, reading R13) equals the oracle's sorted max_occ row, entry by entry; the AEP curve of
