@@ -8,7 +8,8 @@
 // for the slot, reads the 4 rows with one 128-bit LDS each (1 wavefront per row) and accumulates.
 // Prints one JSON line per (S, blocks per SM): rows/s, to compare with microbench_rowpattern.cu
 // (LDG: 1.13e11 rows/s at 12 warps/SM with 2 lanes per row, 1.69e11 with 4 lanes per row).
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather4 microbench_gather4.cu -lcuda
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather4 microbench_gather4.cu
+// (cuTensorMapEncodeTiled through cudaGetDriverEntryPoint: no -lcuda)
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
@@ -119,6 +120,5 @@ int main(int argc, char** argv) {
     run<4>(tm, bps, sms, did, n, k, dout);
     run<8>(tm, bps, sms, did, n, k, dout);
   }
-  // correctness of the gathered data: compare one warp's accumulation with the host
   return 0;
 }
