@@ -86,6 +86,32 @@ def test_elts_per_layer_widths(stream, n_elts):
     assert_bit_identical(gpu_ylt(ds, stream), oracle.run_analysis(ds))
 
 
+@pytest.mark.parametrize("n_elts", [25, 32, 40, 48])
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("ev2", ["1", "0"])
+def test_two_event_step_widths(stream, monkeypatch, n_elts, mode, ev2):
+    """The two-events-per-step pair scan (25-48 ELTs, map modes 0 and 1; ARA_PAIR_EV2=0 keeps one
+    event per step): ragged trials of 0-43 events (every residue of the 8-event chunk and of the
+    event pairs, head and tail singles), a misaligned id pointer, and a second run on the same
+    context -- bit-identical to the oracle, and the launched instantiation is the one asked for."""
+    monkeypatch.setenv("ARA_MAP_MODE", str(mode))
+    monkeypatch.setenv("ARA_PAIR_EV2", ev2)
+    spec = datagen.PRESETS["tiny"].replace(n_elts=n_elts, elts_per_layer=n_elts, n_trials=700,
+                                           k_min=0, k_max=43, seed=31 + n_elts)
+    ds = datagen.generate(spec)
+    want = oracle.run_analysis(ds)
+    ctx = make_ctx(ds, stream)
+    for shift in (0, 3):
+        ev = np.concatenate([np.full(shift, 1, np.uint32), ds.events])
+        off = ds.trial_offsets + np.uint64(shift)
+        ylt = torch.empty((1, ds.n_trials), dtype=torch.float64, device=DEV)
+        ctx.ara_run(to_dev(off, "u64"), to_dev(ev, "u32")[shift:], ylt, flags=ara.ARA_RUN_SYNC)
+        assert_bit_identical(ylt.cpu().numpy(), want)
+        kern = ctx.ara_get_info().last_kernel.decode()
+        assert kern.startswith("pair_scan_kernel<4,") and kern.endswith(", 2>" if ev2 == "1" else ", 1>"), kern
+    ctx.close()
+
+
 def test_ragged_and_misaligned(stream):
     """Variable lengths (0..37 events, empty trials included), a YET slice whose offsets start
     at a non-zero base and whose id pointer is not 32-byte aligned (head/tail paths)."""
