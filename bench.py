@@ -454,6 +454,9 @@ def main():
                     help="N > 1: gather the YLT slices and compute PML/TVaR on every rank (north "
                          "star), or ara_metrics_sharded (histograms all-reduced per pass)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-offload", action="store_true",
+                    help="N > 1: every rank computes PML/TVaR on the gathered YLT and the trials "
+                         "split evenly (default: rank 0 alone, with a lighter trial share)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--json-out", default=None)
@@ -492,22 +495,28 @@ def main():
     if world > 1:  # setup collective: rank 0's ELTs and terms reach every rank (NVLink)
         adist.broadcast_inputs(ds, src=0)
     n_total = spec.n_trials * world if args.scaling == "weak" else spec.n_trials
-    t0, t1 = partition(n_total, rank, world)
-    n_loc = t1 - t0
-    h_off_np = datagen.trial_offsets(spec, t0, n_loc)
-    n_ev = int(h_off_np[-1])
-    h_ids = torch.empty(n_ev, dtype=torch.int32, pin_memory=True)
-    datagen.generate_yet(spec, ds.pool, t0, n_loc, out=h_ids.numpy().view(np.uint32))
-    h_off = torch.from_numpy(h_off_np.view(np.int64)).pin_memory()
-    d_off = h_off.to(dev).view(torch.uint64)
-    d_ids = h_ids.to(dev).view(torch.uint32)
     L = ds.n_layers
     # YLT rows 0..L-1 and, for L > 1, the portfolio-scope row L
     L1 = L + 1 if L > 1 else L
-    d_ylt_buf = torch.empty((L1, n_loc), dtype=torch.float64, device=dev)
-    d_ylt_loc = d_ylt_buf[:L]
+    parts = adist.partition_trials(n_total, world)  # balanced contiguous ranges
+
+    def load_slice(parts):
+        """This rank's YET slice (host, pinned) and its device copies and YLT buffers."""
+        t0, t1 = parts[rank]
+        n_loc = t1 - t0
+        h_off_np = datagen.trial_offsets(spec, t0, n_loc)
+        n_ev = int(h_off_np[-1])
+        h_ids = torch.empty(n_ev, dtype=torch.int32, pin_memory=True)
+        datagen.generate_yet(spec, ds.pool, t0, n_loc, out=h_ids.numpy().view(np.uint32))
+        h_off = torch.from_numpy(h_off_np.view(np.int64)).pin_memory()
+        d_ylt_buf = torch.empty((L1, n_loc), dtype=torch.float64, device=dev)
+        return (n_loc, h_off_np, n_ev, h_ids, h_off, h_off.to(dev).view(torch.uint64),
+                h_ids.to(dev).view(torch.uint32), d_ylt_buf, d_ylt_buf[:L],
+                d_ylt_buf[L] if L > 1 else None)
+
+    (n_loc, h_off_np, n_ev, h_ids, h_off, d_off, d_ids, d_ylt_buf, d_ylt_loc,
+     d_port_loc) = load_slice(parts)
     d_full_buf = torch.empty((L1, n_total), dtype=torch.float64, device=dev)
-    d_port_loc = d_ylt_buf[L] if L > 1 else None
     stream = torch.cuda.current_stream(dev)
     ctx = ara.Context(local, stream)
     ctx.ara_set_precision(args.precision)
@@ -523,7 +532,7 @@ def main():
     def gather():
         if world == 1:
             return d_ylt_buf
-        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L])
+        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L], parts=parts)
         return d_full_buf
 
     def post_metrics(rows):
@@ -535,6 +544,44 @@ def main():
 
     scan_ev = []
     run_flags = ara.ARA_RUN_HOIST if args.hoist else 0
+    # Strong/weak scaling with the gathered YLT: rank 0 alone computes PML/TVaR (every rank holds
+    # the same gathered rows, so one evaluation suffices), and it scans correspondingly fewer
+    # trials so that no rank waits on the others (dist.partition_rank0_offload).  The metrics'
+    # cost in scanned trials, mu, is measured here on the balanced split: one scan per rank and
+    # one metrics call on rank 0, timed with CUDA events; the slices are then regenerated.
+    offload = world > 1 and args.metrics == "gather" and not args.no_offload
+    mu = 0.0
+    if offload:
+        for _ in range(2):
+            ctx.ara_run(d_off, d_ids, d_ylt_loc, flags=run_flags)
+        rows = gather()
+        post_metrics(rows)
+        torch.cuda.synchronize()
+        ta = torch.cuda.Event(enable_timing=True); tb = torch.cuda.Event(enable_timing=True)
+        ta.record(stream)
+        for _ in range(3):
+            ctx.ara_run(d_off, d_ids, d_ylt_loc, flags=run_flags)
+        tb.record(stream)
+        torch.cuda.synchronize()
+        t_trial = ta.elapsed_time(tb) / 3 / max(n_loc, 1)
+        rows = gather()
+        t_met = 0.0
+        if rank == 0:
+            torch.cuda.synchronize()
+            ta.record(stream)
+            for _ in range(3):
+                post_metrics(rows)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            t_met = ta.elapsed_time(tb) / 3
+        t_trial, t_met = adist.max_over_ranks([t_trial, t_met])
+        mu = t_met / t_trial if t_trial > 0 else 0.0
+        parts = adist.partition_rank0_offload(n_total, world, mu)
+        (n_loc, h_off_np, n_ev, h_ids, h_off, d_off, d_ids, d_ylt_buf, d_ylt_loc,
+         d_port_loc) = load_slice(parts)
+        if rank == 0:
+            log(f"[bench] metrics on rank 0 = {t_met:.3f} ms = {mu:.0f} trials of scanning; "
+                f"trials per rank {[b - a for a, b in parts]}")
 
     def step(timed: bool):
         if timed:
@@ -550,7 +597,10 @@ def main():
                 ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
                 res.append(adist.sharded_metrics(ctx, d_port_loc, n_total, P))
             return res
-        return post_metrics(gather())  # A9 (+ portfolio scope)
+        rows = gather()
+        if offload and rank != 0:
+            return None
+        return post_metrics(rows)  # A9 (+ portfolio scope)
 
     for _ in range(args.warmup):
         step(False)
@@ -574,7 +624,7 @@ def main():
     launches = ctx.kernel_launches - launches0
     # the last timed step's YLT (gathered over the ranks), for the parity check below
     if world > 1 and args.metrics == "sharded" and not args.no_parity:  # not gathered in steps
-        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L])
+        adist.gather_ylt(d_ylt_loc, n_total, out=d_full_buf[:L], parts=parts)
     last_ylt = (d_full_buf if world > 1 else d_ylt_buf)[:L].cpu().numpy() if rank == 0 else None
     ms = e0.elapsed_time(e1) / args.steps
     scan_ms = statistics.mean(a.elapsed_time(b) for a, b in scan_ev)
@@ -618,7 +668,9 @@ def main():
                     ctx.ara_portfolio_ylt(d_ylt_loc, d_port_loc)
                     adist.sharded_metrics(ctx, d_port_loc, n_total, P)
             else:
-                post_metrics(gather())
+                rows = gather()
+                if not (offload and rank != 0):
+                    post_metrics(rows)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - tt)
         t_e2e = statistics.median(ts)
@@ -662,6 +714,10 @@ def main():
                            f" per GPU ({n_total} trials in total)"
                            if world > 1 and args.scaling == "weak" else ""), "layers": L, "elts_per_layer": E,
                        "trials": n_total, "trials_per_gpu": n_loc,
+                       "trials_by_rank": [b - a for a, b in parts] if world > 1 else None,
+                       "metrics_on": ("rank 0 (rank 0 scans fewer trials: the metrics cost "
+                                      f"{mu:.0f} trials of scanning, measured)" if offload
+                                      else "every rank" if world > 1 else "the GPU"),
                        "events_per_trial": spec.k_min,
                        "parallelism": f"trial-sharded x{world}, {args.scaling} scaling "
                                       + ("(PML/TVaR by sharded radix select, histograms "

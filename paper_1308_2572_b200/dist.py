@@ -34,6 +34,20 @@ def shard_range(n_trials: int, rank: int, world: int) -> Tuple[int, int]:
     return partition_trials(n_trials, world)[rank]
 
 
+def partition_rank0_offload(n_trials: int, world: int, mu: float) -> List[Tuple[int, int]]:
+    """Contiguous trial ranges when rank 0 alone computes PML/TVaR after the all-gather, which
+    costs it as much time as scanning ``mu`` trials: rank 0 takes n0 = (n + mu) / R - mu trials
+    (never more than the balanced share, never fewer than 0) and the other ranks split the rest
+    as partition_trials does, so every rank's step (scan, plus the metrics on rank 0) takes the
+    same time.  mu <= 0 or R = 1 gives partition_trials."""
+    if world <= 1 or not mu or mu <= 0:
+        return partition_trials(n_trials, world)
+    n0 = int(round((n_trials + mu) / world - mu))
+    n0 = min(max(n0, 0), n_trials // world)
+    rest = partition_trials(n_trials - n0, world - 1)
+    return [(0, n0)] + [(n0 + a, n0 + b) for a, b in rest]
+
+
 def _dev_for(dist, like=None):
     import torch
     if dist.get_backend() == "nccl":
@@ -67,22 +81,24 @@ def broadcast_inputs(ds, src: int = 0):
     return ds
 
 
-def gather_ylt(ylt_local, n_trials: int, out=None):
+def gather_ylt(ylt_local, n_trials: int, out=None, parts=None):
     """All-gather the [L, n_local] YLT slices of every rank into the full [L, n_trials] YLT
     (layer-major rows, trials in rank order).  ``ylt_local`` / ``out`` are tensors on the
-    backend's device."""
+    backend's device; ``parts`` = every rank's trial range (default partition_trials)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size()
     L = ylt_local.shape[0]
     if out is None:
         out = torch.empty((L, n_trials), dtype=ylt_local.dtype, device=ylt_local.device)
-    parts = partition_trials(n_trials, world)
+    if parts is None:
+        parts = partition_trials(n_trials, world)
+    assert len(parts) == world and parts[-1][1] == n_trials
     m = max(b - a for a, b in parts)
     equal = all(b - a == m for a, b in parts)
     nccl = dist.get_backend() == "nccl"
     if not nccl and ylt_local.is_cuda:  # gloo: stage through host memory
-        host = gather_ylt(ylt_local.cpu(), n_trials)
+        host = gather_ylt(ylt_local.cpu(), n_trials, parts=parts)
         out.copy_(host)
         return out
     for l in range(L):

@@ -186,8 +186,9 @@ def test_run_host_error_writes_nothing(flags):
 def test_two_ranks_sharded_path():
     """The multi-GPU path of bench.py with 2 processes sharing this GPU (gloo): each rank scans
     its trial slice through libara, the slices are all-gathered (dist.gather_ylt) and PML/TVaR
-    computed (ara_metrics_rows); rank 0 compares the gathered YLT of the last timed step with
-    the single-process oracle over the whole workload, every entry."""
+    computed (ara_metrics_rows) on rank 0, which scans fewer trials to make up for it; rank 0
+    compares the gathered YLT of the last timed step with the single-process oracle over the
+    whole workload, every entry."""
     env = dict(os.environ, ARA_BENCH_SAME_DEVICE="1", MASTER_ADDR="127.0.0.1")
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
@@ -199,7 +200,11 @@ def test_two_ranks_sharded_path():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong"
-    assert d["config"]["trials"] == 100_000 and d["config"]["trials_per_gpu"] == 50_000
+    # rank 0 computes PML/TVaR alone and scans fewer trials (dist.partition_rank0_offload)
+    by_rank = d["config"]["trials_by_rank"]
+    assert d["config"]["trials"] == 100_000 and sum(by_rank) == 100_000
+    assert by_rank[0] == d["config"]["trials_per_gpu"] and by_rank[0] <= 50_000 <= by_rank[1]
+    assert d["config"]["metrics_on"].startswith("rank 0")
     p = d["parity"]
     assert p["pass"] and p["ylt_mismatches"] == 0 and p["ylt_n"] == 100_000 and p["pml_exact"]
 
