@@ -49,6 +49,21 @@ using namespace scan_detail;
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Bounds-checking debug builds (-DARA_DEBUG_BOUNDS, a tuning-library variant; compute-sanitizer
+// is not available on every pool): every row index, trial range and YLT index is checked and a
+// violation traps (a sticky launch error).  Product builds compile the checks away.
+#ifdef ARA_DEBUG_BOUNDS
+__constant__ uint64_t c_dbg_rows;  // rows of the store this launch reads
+#define ARA_DBG_CHECK(cond) \
+    do {                    \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define ARA_DBG_CHECK(cond) \
+    do {                    \
+    } while (0)
+#endif
+
 
 template <int N>
 struct ScaledTerms {
@@ -180,6 +195,7 @@ template <int G, int CH, bool ILV>
 __device__ __forceinline__ void gather2(const double *__restrict__ my_rows, uint32_t stride,
                                         uint32_t idx, Chunk<double> (&r)[CH])
 {
+    ARA_DBG_CHECK(idx < c_dbg_rows);
     const double *p = my_rows + (size_t)idx * stride;
 #pragma unroll
     for (int k = 0; k < CH; ++k) load_row_chunk(p + (ILV ? 4 * G : 4) * k, r[k]);
@@ -277,6 +293,8 @@ __device__ __forceinline__ void pair_body(const ScanLaunch &s, const uint32_t *_
             }
             const uint64_t beg = s.offsets[t] - base;
             const uint64_t k = s.offsets[t + 1] - base - beg;
+            ARA_DBG_CHECK(t < s.n_trials && t < s.ylt_ld && s.offsets[t] >= base &&
+                          beg + k <= s.offsets[s.n_trials] - base);
             const uint32_t *const tr = s.ids + beg;  // the trial's event ids
             TrialState st{0.0, 0.0, 0.0, 0.0};
             double own = 0.0;
@@ -417,6 +435,12 @@ cudaError_t launch_pair(const DeviceStore &st, const ScanLaunch &s, int sm_count
     ScanLaunch sl = s;
     sl.zero_base = MM ? st.zero_base_direct : st.zero_base;
     sl.bitmap_log2 = kBitmapLog2Scan;
+#ifdef ARA_DEBUG_BOUNDS
+    const uint64_t rows_lim = (uint64_t)sl.zero_base + kZeroRows;
+    e = cudaMemcpyToSymbolAsync(c_dbg_rows, &rows_lim, sizeof(rows_lim), 0,
+                                cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+#endif
     static const std::string name = kernel_name("pair_scan_kernel", G, CH, MINB, MM, X, EV);
     t_last_kernel = name.c_str();
     kern<<<(unsigned)blocks, kScanThreads, smem, stream>>>(
